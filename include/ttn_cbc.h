@@ -1,0 +1,134 @@
+/*
+ * ttn_cbc.h — C ABI of libttncbc.so: Cholesky-based compression (CBC) of a tree tensor
+ * network operator (TTNO) applied to a tree tensor network state (TTNS) on B200 (sm_100a).
+ *
+ * Method: M. Milbradt, S. Sun, C. B. Mendl, J. Gray, G. K.-L. Chan, arXiv 2601.19650,
+ * "Efficient Application of Tensor Network Operators to Tensor Network States".
+ * Citations are PAPER.md line numbers (P:n) with the section / equation they fall in.
+ *
+ * Conventions (all calls):
+ *  - Complex numbers are ttn_c128 = {double re, im} (layout of C99 double _Complex and
+ *    cuDoubleComplex).  All tensors are dense, row-major (last index fastest).
+ *  - Every call returns a ttn_status.  Nothing throws across the ABI.  On error every
+ *    output handle is set to NULL and ttn_last_error(ctx) describes the failure.
+ *  - A ttn_ctx binds one CUDA device and one CUDA stream.  All device work of a call is
+ *    enqueued on that stream; calls that return host values synchronise it.  A ctx is not
+ *    thread-safe; distinct ctxs may be used concurrently.
+ *  - Handles (ttn) are immutable, library-owned and device-resident.  The caller destroys
+ *    every handle it receives (ttn_destroy) before destroying the ctx that created it.
+ */
+#ifndef TTN_CBC_H
+#define TTN_CBC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TTN_API __attribute__((visibility("default")))
+#else
+#define TTN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TTN_OK = 0,
+  TTN_ERR_ARG = 1,          /* NULL pointer, max_bond < 1, tol outside [0,1), bad node id   */
+  TTN_ERR_TOPOLOGY = 2,     /* not a single rooted tree; op and state parent arrays differ  */
+  TTN_ERR_SHAPE = 3,        /* bond / physical-dimension mismatch across an edge or op-state */
+  TTN_ERR_OOM = 4,          /* device or pinned-host allocation failed                       */
+  TTN_ERR_CUDA = 5,         /* a CUDA runtime call or kernel launch failed                   */
+  TTN_ERR_NUMERIC = 6,      /* non-finite values, eigensolver / Cholesky breakdown            */
+  TTN_ERR_UNSUPPORTED = 7   /* a size beyond the compiled limits (see ttn_last_error)        */
+} ttn_status;
+
+typedef enum { TTN_STATE = 0, TTN_OPERATOR = 1 } ttn_kind;
+
+typedef struct { double re, im; } ttn_c128;
+
+typedef struct ttn_ctx_s* ttn_ctx;
+typedef struct ttn_s* ttn;
+
+/* Per-apply report (§IV.B metrics; SPEC ApplyReport).            */
+typedef struct {
+  double norm;                 /* ||phi|| = ||T'_root||_F (non-root tensors are isometries) */
+  double discarded_weight_sum; /* sum over all compress steps of the dropped eigenvalues     */
+  int64_t max_bond;            /* largest bond of the result                                */
+  int64_t peak_entries;        /* largest number of complex entries held by one intermediate */
+  double seconds;              /* host wall time of the call                                */
+  double flops_algorithmic;    /* 8 * complex MACs of every contraction / Gram / factor GEMM */
+  int32_t rank_fallbacks;      /* Eq. 13 QRs that fell back from CholeskyQR2 (rank-deficient) */
+  int32_t host_syncs;          /* stream synchronisations taken for data-dependent ranks     */
+} ttn_cbc_report;
+
+/* ---------------------------------------------------------------- context             */
+/* Create a context on CUDA device `device` using stream `cuda_stream` (a cudaStream_t;
+ * NULL = the legacy default stream).  Device memory comes from a cudaMallocAsync pool on
+ * that stream.                                                                           */
+TTN_API ttn_status ttn_ctx_create(int device, void* cuda_stream, ttn_ctx* out);
+TTN_API ttn_status ttn_ctx_destroy(ttn_ctx ctx);
+/* Text of the last error on this ctx; valid until the next call on the ctx.             */
+TTN_API const char* ttn_last_error(ttn_ctx ctx);
+/* Library version string, e.g. "ttncbc 0.1 sm_100a".                                    */
+TTN_API const char* ttn_version(void);
+
+/* ---------------------------------------------------------------- tree tensor networks */
+/* Create a TTNS (kind = TTN_STATE, Eq. 2) or TTNO (TTN_OPERATOR, Eq. 4).
+ *  n_nodes   number of sites L >= 1
+ *  parent    parent[i] of node i; exactly one -1 (the root).  Children of a node are
+ *            ordered by ascending node id, which fixes the leg order below.
+ *  phys_dim  d_i >= 1 ("d_i can be 1")
+ *  bond      bond[i] = extent of edge (i, parent[i]) >= 1; ignored for the root (extent 1)
+ *  data      data[i] points to node i's tensor, row-major in the ABI leg order
+ *              state    : [d_i, bond(parent edge), bond(child c1), bond(child c2), ...]
+ *              operator : [d_i (out sigma'), d_i (in sigma), bond(parent), bond(c1), ...]
+ *            The root's parent leg is present with extent 1; leaves have no child
+ *            legs.  MPS / MPO: parent[i] = i-1, site i's tensor is [d, a_left, a_right]
+ *            (Eq. 3).
+ *  data_on_device  0: data[i] are host pointers (copied H2D); 1: device pointers (D2D).
+ * The data is copied; the caller keeps ownership of its buffers.
+ * Errors: TOPOLOGY (no single root, cycle), ARG (NULL, d < 1, bond < 1).               */
+TTN_API ttn_status ttn_create(ttn_ctx ctx, ttn_kind kind, int32_t n_nodes, const int32_t* parent,
+                      const int32_t* phys_dim, const int64_t* bond,
+                      const ttn_c128* const* data, int data_on_device, ttn* out);
+TTN_API ttn_status ttn_destroy(ttn t);
+TTN_API ttn_status ttn_n_nodes(ttn t, int32_t* out);
+/* Shape of node `node` in ABI leg order; dims must hold >= 16 entries.                   */
+TTN_API ttn_status ttn_node_shape(ttn t, int32_t node, int32_t* ndim, int64_t* dims);
+/* Copy node `node` (ABI leg order) to host memory `host_out` with room for
+ * `capacity_elems` complex entries (ARG if too small).  Synchronises the ctx stream.    */
+TTN_API ttn_status ttn_get_tensor(ttn_ctx ctx, ttn t, int32_t node, ttn_c128* host_out, size_t capacity_elems);
+
+/* ---------------------------------------------------------------- CBC                  */
+/* phi ~= O |psi> by CBC (§III.B, Eqs. 10-14; tensor train §III.A,
+ * Eqs. 5-9, is the special case of a chain rooted at site 0).
+ *  op, state  TTNO and TTNS on the same parent array and physical dimensions.
+ *  max_bond   D-bar >= 1: every bond of the result is <= max_bond.
+ *  tol        relative singular-value cutoff in [0, 1): directions with
+ *             sigma_j <= tol * sigma_1 are dropped ("setting a tolerance for the SVD";
+ *             reading A3 in DESIGN.md).  tol = 0 keeps min(max_bond, numerical rank).
+ *  out        new TTNS, same topology; non-root tensors are isometries toward the root
+ *             (Q of Eq. 13), the root carries the norm; no renormalisation.
+ *  rep        optional report (may be NULL).
+ * Errors: TOPOLOGY, SHAPE, ARG, NUMERIC, OOM, CUDA.                                      */
+TTN_API ttn_status cbc_apply(ttn_ctx ctx, ttn op, ttn state, int64_t max_bond, double tol,
+                     ttn* out, ttn_cbc_report* rep);
+/* n independent applies in one level-synchronous schedule (all instances share the parent
+ * array and physical dimensions; bonds may differ).  outs[n]; reps[n] may be NULL.       */
+TTN_API ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const ttn* states,
+                           int64_t max_bond, double tol, ttn* outs, ttn_cbc_report* reps);
+
+/* <a|b>, conjugate-linear in a, by a leaves-to-root environment sweep; a and b share the
+ * parent array and physical dimensions, bonds may differ.  Synchronises the stream.      */
+TTN_API ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out);
+/* Batched overlaps <a_j|b_j>, j < n.                                                      */
+TTN_API ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b, ttn_c128* out);
+/* sqrt(Re <a|a>).                                                                         */
+TTN_API ttn_status ttn_norm(ttn_ctx ctx, ttn a, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTN_CBC_H */

@@ -1,0 +1,171 @@
+"""B200-native CBC (arXiv 2601.19650): Python binding of libttncbc.so.
+
+Same names as the C ABI (include/ttn_cbc.h): ttn_ctx_create, ttn_create, cbc_apply,
+cbc_apply_batch, ttn_overlap, ttn_norm, ttn_get_tensor, ...  The binding only marshals
+arguments; every step of the hot path runs in the CUDA kernels of csrc/.  PyTorch is used
+(optionally) for the CUDA stream and for device-resident inputs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import TTN_OPERATOR, TTN_STATE, TTNError
+
+__all__ = ["Context", "TTN", "ttn_ctx_create", "ttn_create", "cbc_apply", "cbc_apply_batch", "ttn_overlap",
+           "ttn_overlap_batch", "ttn_norm", "ttn_get_tensor", "ttn_version", "TTN_STATE", "TTN_OPERATOR",
+           "TTNError", "lib_path"]
+
+lib_path = L.LIB_PATH
+
+
+def ttn_version() -> str:
+    return L.load().ttn_version().decode()
+
+
+class Context:
+    """A ttn_ctx bound to one device and one CUDA stream (default: torch's current stream)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        lib = L.load()
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device).cuda_stream
+            except Exception:
+                stream = None
+        self.device = device
+        self.stream = stream or 0
+        h = C.c_void_p()
+        L.check(None, lib.ttn_ctx_create(int(device), C.c_void_p(self.stream), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            L.load().ttn_ctx_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def ttn_ctx_create(device: int = 0, stream: Optional[int] = None) -> Context:
+    return Context(device, stream)
+
+
+class TTN:
+    """Handle of a device-resident TTNS / TTNO (immutable)."""
+
+    def __init__(self, ctx: Context, h: C.c_void_p, kind: int):
+        self.ctx, self.h, self.kind = ctx, h, kind
+
+    def destroy(self):
+        if self.h:
+            L.load().ttn_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    @property
+    def n_nodes(self) -> int:
+        v = C.c_int32()
+        L.check(self.ctx.h, L.load().ttn_n_nodes(self.h, C.byref(v)))
+        return v.value
+
+    def shape(self, node: int):
+        nd = C.c_int32()
+        dims = (C.c_int64 * 16)()
+        L.check(self.ctx.h, L.load().ttn_node_shape(self.h, node, C.byref(nd), dims))
+        return tuple(dims[i] for i in range(nd.value))
+
+    def bonds(self) -> List[int]:
+        off = 1 if self.kind == TTN_STATE else 2
+        return [self.shape(i)[off] for i in range(self.n_nodes)]
+
+    def get(self, node: int) -> np.ndarray:
+        return ttn_get_tensor(self.ctx, self, node)
+
+    def tensors(self) -> List[np.ndarray]:
+        return [self.get(i) for i in range(self.n_nodes)]
+
+
+def ttn_create(ctx: Context, kind: int, parent: Sequence[int], phys: Sequence[int], bond: Sequence[int],
+               tensors: Sequence, on_device: Optional[bool] = None) -> TTN:
+    """tensors: numpy complex128 arrays (host) or torch complex128 CUDA tensors (device)."""
+    n = len(parent)
+    keep = []
+    ptrs = (C.c_void_p * n)()
+    dev = on_device
+    for i, t in enumerate(tensors):
+        if hasattr(t, "data_ptr"):  # torch tensor
+            import torch
+            assert t.dtype == torch.complex128 and t.is_contiguous()
+            ptrs[i] = t.data_ptr()
+            dev = True if dev is None else dev
+            keep.append(t)
+        else:
+            a = L.host_c128(t)
+            keep.append(a)
+            ptrs[i] = a.ctypes.data
+            dev = False if dev is None else dev
+    h = C.c_void_p()
+    L.check(ctx.h, L.load().ttn_create(ctx.h, int(kind), n, L.as_i32(parent), L.as_i32(phys), L.as_i64(bond),
+                                       ptrs, int(bool(dev)), C.byref(h)))
+    return TTN(ctx, h, kind)
+
+
+def ttn_get_tensor(ctx: Context, t: TTN, node: int) -> np.ndarray:
+    shp = t.shape(node)
+    out = np.empty(shp, dtype=np.complex128)
+    L.check(ctx.h, L.load().ttn_get_tensor(ctx.h, t.h, node, C.c_void_p(out.ctypes.data), out.size))
+    return out
+
+
+def cbc_apply(ctx: Context, op: TTN, state: TTN, max_bond: int, tol: float = 0.0):
+    """Returns (new TTNS handle, report dict)."""
+    out = C.c_void_p()
+    rep = L.Report()
+    L.check(ctx.h, L.load().cbc_apply(ctx.h, op.h, state.h, int(max_bond), float(tol), C.byref(out), C.byref(rep)))
+    return TTN(ctx, out, TTN_STATE), rep.as_dict()
+
+
+def cbc_apply_batch(ctx: Context, ops: Sequence[TTN], states: Sequence[TTN], max_bond: int, tol: float = 0.0):
+    n = len(ops)
+    po = (C.c_void_p * n)(*[o.h.value for o in ops])
+    ps = (C.c_void_p * n)(*[s.h.value for s in states])
+    outs = (C.c_void_p * n)()
+    reps = (L.Report * n)()
+    L.check(ctx.h, L.load().cbc_apply_batch(ctx.h, n, po, ps, int(max_bond), float(tol), outs, reps))
+    return [TTN(ctx, C.c_void_p(outs[i]), TTN_STATE) for i in range(n)], [reps[i].as_dict() for i in range(n)]
+
+
+def ttn_overlap(ctx: Context, a: TTN, b: TTN) -> complex:
+    v = L.c128()
+    L.check(ctx.h, L.load().ttn_overlap(ctx.h, a.h, b.h, C.byref(v)))
+    return complex(v.re, v.im)
+
+
+def ttn_overlap_batch(ctx: Context, a: Sequence[TTN], b: Sequence[TTN]) -> List[complex]:
+    n = len(a)
+    pa = (C.c_void_p * n)(*[x.h.value for x in a])
+    pb = (C.c_void_p * n)(*[x.h.value for x in b])
+    out = (L.c128 * n)()
+    L.check(ctx.h, L.load().ttn_overlap_batch(ctx.h, n, pa, pb, out))
+    return [complex(out[i].re, out[i].im) for i in range(n)]
+
+
+def ttn_norm(ctx: Context, a: TTN) -> float:
+    v = C.c_double()
+    L.check(ctx.h, L.load().ttn_norm(ctx.h, a.h, C.byref(v)))
+    return v.value

@@ -1,0 +1,216 @@
+// extern "C" entry points of libttncbc (include/ttn_cbc.h).  Every call converts
+// exceptions to a ttn_status and records the message on the context.
+#include "runtime.h"
+
+#include <cstring>
+#include <new>
+#include <vector>
+
+using namespace tcbc;
+
+namespace {
+
+template <typename F>
+ttn_status guard(ttn_ctx ctx, F&& f) {
+  try {
+    f();
+    return TTN_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return TTN_ERR_OOM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return TTN_ERR_CUDA;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ttn_version(void) { return "ttncbc 0.1 sm_100a (DMMA complex-FP64)"; }
+
+ttn_status ttn_ctx_create(int device, void* cuda_stream, ttn_ctx* out) {
+  if (!out) return TTN_ERR_ARG;
+  *out = nullptr;
+  ttn_ctx_s* c = new (std::nothrow) ttn_ctx_s();
+  if (!c) return TTN_ERR_OOM;
+  ttn_status s = guard(nullptr, [&] {
+    int n = 0;
+    TTN_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw Error(TTN_ERR_ARG, "bad device id");
+    TTN_CUDA(cudaSetDevice(device));
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    c->stager = new RingStager(c->stream);
+    c->ensure_small(1 << 20);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  if (s != TTN_OK) {
+    delete c->stager;
+    delete c;
+    return s;
+  }
+  *out = c;
+  return TTN_OK;
+}
+
+ttn_status ttn_ctx_destroy(ttn_ctx ctx) {
+  if (!ctx) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->scratch.release();
+  ctx->env.release();
+  delete ctx->stager;
+  if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
+  delete ctx;
+  return TTN_OK;
+}
+
+const char* ttn_last_error(ttn_ctx ctx) { return ctx ? ctx->last_error.c_str() : "NULL context"; }
+
+ttn_status ttn_create(ttn_ctx ctx, ttn_kind kind, int32_t n_nodes, const int32_t* parent, const int32_t* phys_dim,
+                      const int64_t* bond, const ttn_c128* const* data, int data_on_device, ttn* out) {
+  if (!ctx || !out) return TTN_ERR_ARG;
+  *out = nullptr;
+  DeviceGuard g(ctx->device);
+  ttn_s* t = nullptr;
+  ttn_status s = guard(ctx, [&] {
+    if (!parent || !phys_dim || !bond || !data) throw Error(TTN_ERR_ARG, "NULL argument");
+    if (kind != TTN_STATE && kind != TTN_OPERATOR) throw Error(TTN_ERR_ARG, "bad kind");
+    t = new ttn_s();
+    t->ctx = ctx;
+    t->kind = kind;
+    build_topology(t, parent, n_nodes);
+    t->phys.assign(phys_dim, phys_dim + n_nodes);
+    t->bond.assign(bond, bond + n_nodes);
+    for (int i = 0; i < n_nodes; ++i) {
+      if (t->phys[i] < 1) throw Error(TTN_ERR_ARG, "phys_dim must be >= 1");
+      if (i != t->root && t->bond[i] < 1) throw Error(TTN_ERR_ARG, "bond must be >= 1");
+      if (!data[i]) throw Error(TTN_ERR_ARG, "NULL tensor pointer");
+    }
+    t->bond[t->root] = 1;
+    finalize_shapes(t);
+    TTN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t->data), sizeof(cplx) * std::max<int64_t>(t->total, 1),
+                             ctx->stream));
+    for (int i = 0; i < n_nodes; ++i) {
+      int64_t e = 1;
+      for (auto x : t->shape[i]) e *= x;
+      TTN_CUDA(cudaMemcpyAsync(t->node(i), data[i], sizeof(cplx) * e,
+                               data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (!data_on_device) ctx->sync();   // host buffers may be pageable: finish before returning
+  });
+  if (s != TTN_OK) {
+    if (t) {
+      if (t->data) cudaFreeAsync(t->data, ctx->stream);
+      delete t;
+    }
+    return s;
+  }
+  *out = t;
+  return TTN_OK;
+}
+
+ttn_status ttn_destroy(ttn t) {
+  if (!t) return TTN_ERR_ARG;
+  DeviceGuard g(t->ctx->device);
+  free_ttn(t);
+  return TTN_OK;
+}
+
+ttn_status ttn_n_nodes(ttn t, int32_t* out) {
+  if (!t || !out) return TTN_ERR_ARG;
+  *out = t->n;
+  return TTN_OK;
+}
+
+ttn_status ttn_node_shape(ttn t, int32_t node, int32_t* ndim, int64_t* dims) {
+  if (!t || !ndim || !dims || node < 0 || node >= t->n) return TTN_ERR_ARG;
+  const auto& s = t->shape[node];
+  if (s.size() > 16) return TTN_ERR_UNSUPPORTED;
+  *ndim = (int32_t)s.size();
+  for (size_t i = 0; i < s.size(); ++i) dims[i] = s[i];
+  return TTN_OK;
+}
+
+ttn_status ttn_get_tensor(ttn_ctx ctx, ttn t, int32_t node, ttn_c128* host_out, size_t capacity_elems) {
+  if (!ctx || !t || !host_out) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    if (node < 0 || node >= t->n) throw Error(TTN_ERR_ARG, "bad node id");
+    int64_t e = 1;
+    for (auto x : t->shape[node]) e *= x;
+    if ((size_t)e > capacity_elems) throw Error(TTN_ERR_ARG, "output buffer too small");
+    TTN_CUDA(cudaMemcpyAsync(host_out, t->node(node), sizeof(cplx) * e, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
+ttn_status cbc_apply(ttn_ctx ctx, ttn op, ttn state, int64_t max_bond, double tol, ttn* out, ttn_cbc_report* rep) {
+  if (!ctx || !out) return TTN_ERR_ARG;
+  return cbc_apply_batch(ctx, 1, &op, &state, max_bond, tol, out, rep);
+}
+
+ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const ttn* states, int64_t max_bond, double tol,
+                           ttn* outs, ttn_cbc_report* reps) {
+  if (!ctx || !ops || !states || !outs || n < 1) return TTN_ERR_ARG;
+  for (int i = 0; i < n; ++i) outs[i] = nullptr;
+  DeviceGuard g(ctx->device);
+  std::vector<ttn_s*> res(n, nullptr);
+  ttn_status s = guard(ctx, [&] {
+    std::vector<const ttn_s*> o(ops, ops + n), st(states, states + n);
+    cbc_apply_impl(ctx, n, o.data(), st.data(), max_bond, tol, res.data(), reps);
+  });
+  if (s != TTN_OK) {
+    for (auto* r : res) free_ttn(r);
+    cudaGetLastError();
+    return s;
+  }
+  for (int i = 0; i < n; ++i) outs[i] = res[i];
+  return TTN_OK;
+}
+
+ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b, ttn_c128* out) {
+  if (!ctx || !a || !b || !out || n < 1) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    std::vector<const ttn_s*> x(a, a + n), y(b, b + n);
+    std::vector<cplx> r(n);
+    overlap_impl(ctx, n, x.data(), y.data(), r.data());
+    for (int i = 0; i < n; ++i) out[i] = ttn_c128{r[i].x, r[i].y};
+  });
+}
+
+ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out) { return ttn_overlap_batch(ctx, 1, &a, &b, out); }
+
+ttn_status ttn_norm(ttn_ctx ctx, ttn a, double* out) {
+  if (!out) return TTN_ERR_ARG;
+  ttn_c128 v;
+  ttn_status s = ttn_overlap(ctx, a, a, &v);
+  if (s != TTN_OK) return s;
+  *out = v.re > 0 ? std::sqrt(v.re) : 0.0;
+  return TTN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,533 @@
+// CBC driver: the level-synchronous schedule of PAPER.md §III.B over a batch of
+// independent instances (same parent array), every stage one set of grouped launches.
+//
+//   up-sweep    (Eq. 10)  deepest level first; X = T O prod_c L^{[c]}
+//   down-sweep  (Eq. 11)  root level first;    Y = T O L^{[(p,i)]} prod_{c!=k} L^{[c]}
+//   compress       Gram (X^H X or X X^H) -> top-k eigenpairs -> factor
+//   final sweep (Eqs. 12-14) deepest first: Z = T O prod_c R^{[c]};
+//               S = Z L^{[(p,i)]T}; Q = CholeskyQR2(S); T' = Q; R^{[i]} = Q^H Z
+//   assembly          T'_root = Z_root
+// Host synchronisation: once per compress level (data-dependent ranks) and once per final
+// level (Cholesky pivot flags).
+#include "contract.h"
+#include "runtime.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <map>
+
+namespace tcbc {
+
+namespace {
+
+struct Fac {
+  cplx* p = nullptr;   // [k, a, b] row-major
+  int64_t k = 0, a = 0, b = 0;
+};
+
+constexpr double kRankFloor = 1e-13;   // reading A4: lambda_j <= 1e-13 lambda_1 is numerically zero
+constexpr double kCholTol = 1e-13;     // relative pivot threshold of CholeskyQR (rank flag)
+
+// labels of a node contraction
+constexpr int L_SIG = 0, L_SIGP = 1, L_A = 10, L_B = 30, L_F = 50;
+
+struct CompressJob {
+  const cplx* X;
+  int64_t m, n;
+  Fac* dst;
+  int64_t a, b;      // column legs of X (n = a*b)
+  int inst;
+};
+
+struct QRJob {
+  const cplx* S;     // m x kd
+  int64_t m, kd;
+  cplx* Q;           // m x r output, r = min(m, kd)
+  int inst;
+};
+
+Task node_task(const ttn_s* st, const ttn_s* op, int i, const std::map<int, const Fac*>& facs, int open_leg,
+               cplx* out) {
+  Task t;
+  Operand T;
+  T.ptr = st->node(i);
+  T.dims = st->shape[i];
+  T.labels.push_back(L_SIG);
+  for (size_t l = 0; l + 1 < T.dims.size(); ++l) T.labels.push_back(L_A + (int)l);
+  Operand O;
+  O.ptr = op->node(i);
+  O.dims = op->shape[i];
+  O.labels.push_back(L_SIGP);
+  O.labels.push_back(L_SIG);
+  for (size_t l = 0; l + 2 < O.dims.size(); ++l) O.labels.push_back(L_B + (int)l);
+  t.ops.push_back(T);
+  t.ops.push_back(O);
+  t.out_labels.push_back(L_SIGP);
+  for (auto& kv : facs) {
+    Operand F;
+    F.ptr = kv.second->p;
+    F.dims = {kv.second->k, kv.second->a, kv.second->b};
+    F.labels = {L_F + kv.first, L_A + kv.first, L_B + kv.first};
+    t.ops.push_back(F);
+    t.out_labels.push_back(L_F + kv.first);
+  }
+  t.out_labels.push_back(L_A + open_leg);
+  t.out_labels.push_back(L_B + open_leg);
+  t.out = out;
+  return t;
+}
+
+void check_heev_size(int64_t nn) {
+  if (nn > heev_max_n())
+    throw Error(TTN_ERR_UNSUPPORTED, "compress Gram of order " + std::to_string(nn) + " exceeds the eigensolver limit " +
+                                         std::to_string(heev_max_n()));
+}
+
+// Gram -> eigenpairs -> factor, for every job; synchronises once to read the ranks.
+void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_bond, double tol,
+                    ExecStats& st, std::vector<double>& w_inst, std::vector<double>& flops_inst) {
+  if (jobs.empty()) return;
+  const int nj = (int)jobs.size();
+  std::vector<GemmProblem> grams, fgemm;
+  std::vector<HeevProblem> hp(nj);
+  std::vector<ScaleRowsProblem> sr;
+  int* d_k = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nj));
+  double* d_w = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nj));
+  std::vector<int64_t> kmaxs(nj);
+  for (int j = 0; j < nj; ++j) {
+    CompressJob& J = jobs[j];
+    const int64_t m = J.m, n = J.n, nn = std::min(m, n);
+    check_heev_size(nn);
+    const int64_t kmax = std::min<int64_t>(max_bond, nn);
+    kmaxs[j] = kmax;
+    cplx* G = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
+    GemmProblem g{};
+    if (m >= n) {   // G = X^H X
+      g.A = J.X; g.opA = OP_C; g.lda = n;
+      g.B = J.X; g.opB = OP_N; g.ldb = n;
+      g.M = (int)n; g.N = (int)n; g.K = (int)m;
+    } else {        // K = X X^H
+      g.A = J.X; g.opA = OP_N; g.lda = n;
+      g.B = J.X; g.opB = OP_C; g.ldb = n;
+      g.M = (int)m; g.N = (int)m; g.K = (int)n;
+    }
+    g.C = G; g.ldc = nn;
+    g.alpha = make_double2(1.0, 0.0);
+    g.beta = make_double2(0.0, 0.0);
+    grams.push_back(g);
+    flops_inst[J.inst] += 8.0 * (double)g.M * g.N * g.K;
+    HeevProblem& h = hp[j];
+    h.A = G;
+    h.n = (int)nn;
+    h.kmax = (int)kmax;
+    h.lam = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * kmax));
+    h.Vt = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * kmax * nn));
+    h.k_out = d_k + j;
+    h.w_out = d_w + j;
+    h.work = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * heev_work_doubles((int)nn, (int)kmax)));
+    h.tau = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn));
+    h.tol2 = tol * tol;
+    h.floor_rel = kRankFloor;
+    h.max_bond = (int)std::min<int64_t>(max_bond, INT32_MAX);
+    flops_inst[J.inst] += 8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * kmax);
+    // factor storage (kmax rows; the first k are the factor)
+    J.dst->p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * kmax * n));
+    J.dst->a = J.a;
+    J.dst->b = J.b;
+    if (m >= n) {
+      ScaleRowsProblem s{};
+      s.Vt = h.Vt; s.lam = h.lam; s.F = J.dst->p; s.kmax = (int)kmax; s.n = (int)n;
+      sr.push_back(s);
+    } else {   // F = conj(Vt) X  (U_k^H X)
+      GemmProblem f{};
+      f.A = h.Vt; f.opA = OP_R; f.lda = m;
+      f.B = J.X; f.opB = OP_N; f.ldb = n;
+      f.C = J.dst->p; f.ldc = n;
+      f.M = (int)kmax; f.N = (int)n; f.K = (int)m;
+      f.alpha = make_double2(1.0, 0.0);
+      f.beta = make_double2(0.0, 0.0);
+      fgemm.push_back(f);
+      flops_inst[J.inst] += 8.0 * (double)kmax * n * m;
+    }
+    st.peak_entries = std::max(st.peak_entries, nn * nn);
+  }
+  gemm_batch(ctx, grams, st);
+  launch_heev(hp.data(), nj, *ctx->stager, ctx->stream);
+  if (!sr.empty()) launch_scale_rows(sr.data(), (int)sr.size(), *ctx->stager, ctx->stream);
+  gemm_batch(ctx, fgemm, st);
+  // read ranks and discarded weights
+  ctx->ensure_small(sizeof(int) * nj + sizeof(double) * nj);
+  int* hk = reinterpret_cast<int*>(ctx->hbuf);
+  double* hw = reinterpret_cast<double*>(ctx->hbuf + sizeof(int) * ((nj + 1) & ~1));
+  TTN_CUDA(cudaMemcpyAsync(hk, d_k, sizeof(int) * nj, cudaMemcpyDeviceToHost, ctx->stream));
+  TTN_CUDA(cudaMemcpyAsync(hw, d_w, sizeof(double) * nj, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  for (int j = 0; j < nj; ++j) {
+    if (hk[j] < 1 || hk[j] > kmaxs[j]) throw Error(TTN_ERR_NUMERIC, "eigensolver returned an invalid rank");
+    if (!std::isfinite(hw[j])) throw Error(TTN_ERR_NUMERIC, "non-finite discarded weight (non-finite input?)");
+    jobs[j].dst->k = hk[j];
+    w_inst[jobs[j].inst] += hw[j];
+  }
+}
+
+// CholeskyQR2 of every S (m > kd); Q = I for m <= kd.  Synchronises once for pivot flags.
+int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vector<double>& flops_inst) {
+  if (jobs.empty()) return 0;
+  std::vector<EyeProblem> eyes;
+  std::vector<GemmProblem> g1, g2, g3, g4;
+  std::vector<PotrfProblem> p1, p2;
+  std::vector<TrtriProblem> t1, t2;
+  std::vector<int> tall;
+  int* d_info = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * 2 * jobs.size()));
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    QRJob& J = jobs[j];
+    if (J.m <= J.kd) {
+      eyes.push_back(EyeProblem{J.Q, (int)J.m, (int)J.m, 0});
+      continue;
+    }
+    tall.push_back((int)j);
+    const int64_t m = J.m, k = J.kd;
+    cplx* W = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * k * k));
+    cplx* Li = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * k * k));
+    cplx* Q1 = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * m * k));
+    cplx* W2 = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * k * k));
+    cplx* Li2 = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * k * k));
+    auto gp = [&](const cplx* A, int opA, long long lda, const cplx* B, int opB, long long ldb, cplx* C, int64_t M,
+                  int64_t N, int64_t K) {
+      GemmProblem g{};
+      g.A = A; g.opA = opA; g.lda = lda; g.B = B; g.opB = opB; g.ldb = ldb; g.C = C; g.ldc = N;
+      g.M = (int)M; g.N = (int)N; g.K = (int)K;
+      g.alpha = make_double2(1.0, 0.0);
+      g.beta = make_double2(0.0, 0.0);
+      flops_inst[J.inst] += 8.0 * (double)M * N * K;
+      return g;
+    };
+    g1.push_back(gp(J.S, OP_C, k, J.S, OP_N, k, W, k, k, m));        // W = S^H S
+    p1.push_back(PotrfProblem{W, k, (int)k, 0, d_info + 2 * j, kCholTol});
+    t1.push_back(TrtriProblem{W, Li, k, (int)k, 0});
+    g2.push_back(gp(J.S, OP_N, k, Li, OP_C, k, Q1, m, k, k));        // Q1 = S L^{-H}
+    g3.push_back(gp(Q1, OP_C, k, Q1, OP_N, k, W2, k, k, m));         // W2 = Q1^H Q1
+    p2.push_back(PotrfProblem{W2, k, (int)k, 0, d_info + 2 * j + 1, kCholTol * 1e-2});
+    t2.push_back(TrtriProblem{W2, Li2, k, (int)k, 0});
+    g4.push_back(gp(Q1, OP_N, k, Li2, OP_C, k, J.Q, m, k, k));       // Q = Q1 L2^{-H}
+    flops_inst[J.inst] += 8.0 * 2.0 * (k * k * k / 3.0);
+  }
+  if (!eyes.empty()) launch_eye(eyes.data(), (int)eyes.size(), *ctx->stager, ctx->stream);
+  if (tall.empty()) return 0;
+  gemm_batch(ctx, g1, st);
+  launch_potrf(p1.data(), (int)p1.size(), *ctx->stager, ctx->stream);
+  launch_trtri(t1.data(), (int)t1.size(), *ctx->stager, ctx->stream);
+  gemm_batch(ctx, g2, st);
+  gemm_batch(ctx, g3, st);
+  launch_potrf(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
+  launch_trtri(t2.data(), (int)t2.size(), *ctx->stager, ctx->stream);
+  gemm_batch(ctx, g4, st);
+  ctx->ensure_small(sizeof(int) * 2 * jobs.size());
+  int* hi = reinterpret_cast<int*>(ctx->hbuf);
+  TTN_CUDA(cudaMemcpyAsync(hi, d_info, sizeof(int) * 2 * jobs.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  int fails = 0;
+  for (int j : tall)
+    if (hi[2 * j] != 0 || hi[2 * j + 1] != 0) ++fails;
+  if (fails)
+    throw Error(TTN_ERR_NUMERIC, "CholeskyQR2 of S (Eq. 13) hit a non-positive pivot in " + std::to_string(fails) +
+                                     " node(s): rank-deficient S (fallback not available in this build)");
+  return 0;
+}
+
+}  // namespace
+
+void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts, int64_t max_bond,
+                    double tol, ttn_s** outs, ttn_cbc_report* reps) {
+  auto t0 = std::chrono::steady_clock::now();
+  if (nb <= 0) throw Error(TTN_ERR_ARG, "batch size must be >= 1");
+  if (max_bond < 1) throw Error(TTN_ERR_ARG, "max_bond must be >= 1");
+  if (!(tol >= 0.0 && tol < 1.0)) throw Error(TTN_ERR_ARG, "tol must be in [0, 1)");
+  const ttn_s* ref = sts[0];
+  for (int b = 0; b < nb; ++b) {
+    if (!ops[b] || !sts[b]) throw Error(TTN_ERR_ARG, "NULL handle");
+    if (ops[b]->kind != TTN_OPERATOR || sts[b]->kind != TTN_STATE)
+      throw Error(TTN_ERR_ARG, "cbc_apply expects (operator, state) handles");
+    if (ops[b]->n != ref->n || sts[b]->n != ref->n || ops[b]->parent != ref->parent || sts[b]->parent != ref->parent)
+      throw Error(TTN_ERR_TOPOLOGY, "topology mismatch: parent arrays differ");
+    if (ops[b]->phys != ref->phys || sts[b]->phys != ref->phys)
+      throw Error(TTN_ERR_SHAPE, "leg mismatch: physical dimensions differ");
+  }
+  const int n = ref->n;
+  const int root = ref->root;
+  const auto& ch = ref->children;
+  int maxd = 0;
+  for (int i = 0; i < n; ++i) maxd = std::max(maxd, ref->depth[i]);
+  // A9: up-factors that are read
+  std::vector<char> used(n, 0);
+  {
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return ref->depth[x] < ref->depth[y]; });
+    for (int i : order) {
+      int p = ref->parent[i];
+      if (p < 0) continue;
+      used[i] = (ch[p].size() >= 2) || used[p];
+    }
+  }
+  ctx->env.reset();
+  ctx->scratch.reset();
+  ctx->host_syncs = 0;
+  ExecStats st;
+  std::vector<double> w_inst(nb, 0.0), flops_inst(nb, 0.0);
+  std::vector<Fac> up((size_t)nb * n), down((size_t)nb * n), R((size_t)nb * n);
+  // trivial factor L^{[(-,r)]} = 1 (extent-1 legs)
+  cplx* one = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx)));
+  launch_fill(one, 1, make_double2(1.0, 0.0), ctx->stream);
+  for (int b = 0; b < nb; ++b) down[(size_t)b * n + root] = Fac{one, 1, 1, 1};
+
+  // ---------------- 1. up-sweep (Eq. 10)
+  for (int L = maxd; L >= 1; --L) {
+    std::vector<Task> tasks;
+    std::vector<CompressJob> jobs;
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < n; ++i) {
+        if (ref->depth[i] != L || !used[i]) continue;
+        std::map<int, const Fac*> f;
+        for (size_t l = 0; l < ch[i].size(); ++l) f[1 + (int)l] = &up[(size_t)b * n + ch[i][l]];
+        tasks.push_back(node_task(sts[b], ops[b], i, f, 0, nullptr));
+        jobs.push_back(CompressJob{nullptr, 0, 0, &up[(size_t)b * n + i], sts[b]->shape[i][1], ops[b]->shape[i][2], b});
+      }
+    if (tasks.empty()) continue;
+    ExecStats cs;
+    contract_batch(ctx, tasks, cs);
+    for (size_t j = 0; j < tasks.size(); ++j) {
+      int64_t tot = 1;
+      for (auto d : tasks[j].out_dims) tot *= d;
+      jobs[j].X = tasks[j].out;
+      jobs[j].n = jobs[j].a * jobs[j].b;
+      jobs[j].m = tot / jobs[j].n;
+    }
+    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+    // per-instance flop share of the contraction (uniform tasks per instance)
+    for (auto& J : jobs) flops_inst[J.inst] += cs.flops / (double)jobs.size();
+    st.flops += cs.flops;
+    compress_batch(ctx, jobs, max_bond, tol, st, w_inst, flops_inst);
+    ctx->scratch.reset();
+  }
+
+  // ---------------- 2. down-sweep (Eq. 11)
+  for (int L = 0; L < maxd; ++L) {
+    std::vector<Task> tasks;
+    std::vector<CompressJob> jobs;
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < n; ++i) {
+        if (ref->depth[i] != L) continue;
+        for (size_t lk = 0; lk < ch[i].size(); ++lk) {
+          int k = ch[i][lk];
+          std::map<int, const Fac*> f;
+          f[0] = &down[(size_t)b * n + i];
+          for (size_t l = 0; l < ch[i].size(); ++l)
+            if (l != lk) f[1 + (int)l] = &up[(size_t)b * n + ch[i][l]];
+          tasks.push_back(node_task(sts[b], ops[b], i, f, 1 + (int)lk, nullptr));
+          jobs.push_back(CompressJob{nullptr, 0, 0, &down[(size_t)b * n + k], sts[b]->shape[k][1], ops[b]->shape[k][2], b});
+        }
+      }
+    if (tasks.empty()) continue;
+    ExecStats cs;
+    contract_batch(ctx, tasks, cs);
+    for (size_t j = 0; j < tasks.size(); ++j) {
+      int64_t tot = 1;
+      for (auto d : tasks[j].out_dims) tot *= d;
+      jobs[j].X = tasks[j].out;
+      jobs[j].n = jobs[j].a * jobs[j].b;
+      jobs[j].m = tot / jobs[j].n;
+    }
+    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+    for (auto& J : jobs) flops_inst[J.inst] += cs.flops / (double)jobs.size();
+    st.flops += cs.flops;
+    compress_batch(ctx, jobs, max_bond, tol, st, w_inst, flops_inst);
+    ctx->scratch.reset();
+  }
+
+  // ---------------- output shapes: r_i = min(d_i prod_c r_c, kd_i); root 1
+  std::vector<std::vector<int64_t>> rb(nb, std::vector<int64_t>(n, 1));
+  {
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return ref->depth[x] > ref->depth[y]; });
+    for (int b = 0; b < nb; ++b)
+      for (int i : order) {
+        if (i == root) { rb[b][i] = 1; continue; }
+        int64_t ms = ref->phys[i];
+        for (int c : ch[i]) ms *= rb[b][c];
+        rb[b][i] = std::min<int64_t>(ms, down[(size_t)b * n + i].k);
+      }
+  }
+  for (int b = 0; b < nb; ++b) outs[b] = new_ttn_like(ctx, ref, TTN_STATE, rb[b]);
+
+  // ---------------- 3. final sweep (Eqs. 12-14) and 4. assembly
+  for (int L = maxd; L >= 0; --L) {
+    std::vector<Task> tasks;
+    std::vector<std::pair<int, int>> who;
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < n; ++i) {
+        if (ref->depth[i] != L) continue;
+        std::map<int, const Fac*> f;
+        for (size_t l = 0; l < ch[i].size(); ++l) f[1 + (int)l] = &R[(size_t)b * n + ch[i][l]];
+        cplx* out = (i == root) ? outs[b]->node(i) : nullptr;   // assembly: T'_root = Z_root
+        tasks.push_back(node_task(sts[b], ops[b], i, f, 0, out));
+        who.push_back({b, i});
+      }
+    ExecStats cs;
+    contract_batch(ctx, tasks, cs);
+    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+    for (auto& w : who) flops_inst[w.first] += cs.flops / (double)who.size();
+    st.flops += cs.flops;
+    std::vector<GemmProblem> sg, rg;
+    std::vector<QRJob> qj;
+    std::vector<PermProblem> pq;
+    std::vector<std::pair<size_t, int64_t>> rinfo;
+    for (size_t j = 0; j < tasks.size(); ++j) {
+      const int b = who[j].first, i = who[j].second;
+      if (i == root) continue;
+      const Fac& fd = down[(size_t)b * n + i];
+      const int64_t nz = fd.a * fd.b;
+      int64_t tot = 1;
+      for (auto d : tasks[j].out_dims) tot *= d;
+      const int64_t ms = tot / nz, kd = fd.k, r = rb[b][i];
+      cplx* S = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * kd));
+      GemmProblem g{};   // S = Z Fd^T  (Eq. 12 via Z)
+      g.A = tasks[j].out; g.opA = OP_N; g.lda = nz;
+      g.B = fd.p; g.opB = OP_T; g.ldb = nz;
+      g.C = S; g.ldc = kd;
+      g.M = (int)ms; g.N = (int)kd; g.K = (int)nz;
+      g.alpha = make_double2(1.0, 0.0);
+      g.beta = make_double2(0.0, 0.0);
+      sg.push_back(g);
+      flops_inst[b] += 8.0 * (double)ms * kd * nz;
+      cplx* Q = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * r));
+      qj.push_back(QRJob{S, ms, kd, Q, b});
+      // T'_i = Q in ABI order [d, r, r_c...]: Q viewed as [d, Rc, r] -> [d, r, Rc]
+      const int64_t d = ref->phys[i], Rc = ms / d;
+      PermProblem pp{};
+      pp.src = Q; pp.dst = outs[b]->node(i); pp.rank = 3; pp.conj = 0;
+      pp.dims[0] = d; pp.dims[1] = r; pp.dims[2] = Rc;
+      pp.sstride[0] = Rc * r; pp.sstride[1] = 1; pp.sstride[2] = r;
+      pp.total = d * r * Rc;
+      pq.push_back(pp);
+      // R_i = Q^H Z  (Eq. 14 with Q*, reading A6)
+      Fac& Ri = R[(size_t)b * n + i];
+      Ri.p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * r * nz));
+      Ri.k = r; Ri.a = fd.a; Ri.b = fd.b;
+      GemmProblem h{};
+      h.A = Q; h.opA = OP_C; h.lda = r;
+      h.B = tasks[j].out; h.opB = OP_N; h.ldb = nz;
+      h.C = Ri.p; h.ldc = nz;
+      h.M = (int)r; h.N = (int)nz; h.K = (int)ms;
+      h.alpha = make_double2(1.0, 0.0);
+      h.beta = make_double2(0.0, 0.0);
+      rg.push_back(h);
+      flops_inst[b] += 8.0 * (double)r * nz * ms;
+    }
+    gemm_batch(ctx, sg, st);
+    qr_batch(ctx, qj, st, flops_inst);
+    if (!pq.empty()) launch_permute(pq.data(), (int)pq.size(), *ctx->stager, ctx->stream);
+    gemm_batch(ctx, rg, st);
+    ctx->scratch.reset();
+  }
+
+  // ---------------- report: ||phi|| = ||T'_root||_F
+  std::vector<SumsqProblem> sq(nb);
+  double* d_sq = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nb));
+  for (int b = 0; b < nb; ++b) {
+    sq[b].x = outs[b]->node(root);
+    sq[b].len = 1;
+    for (auto d : outs[b]->shape[root]) sq[b].len *= d;
+    sq[b].out = d_sq + b;
+  }
+  launch_sumsq(sq.data(), nb, *ctx->stager, ctx->stream);
+  ctx->ensure_small(sizeof(double) * nb);
+  double* hs = reinterpret_cast<double*>(ctx->hbuf);
+  TTN_CUDA(cudaMemcpyAsync(hs, d_sq, sizeof(double) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  TTN_CUDA(cudaGetLastError());
+  ctx->scratch.reset();
+  ctx->env.reset();
+  double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (reps) {
+    for (int b = 0; b < nb; ++b) {
+      ttn_cbc_report& r = reps[b];
+      r.norm = std::sqrt(hs[b]);
+      r.discarded_weight_sum = w_inst[b];
+      r.max_bond = 1;
+      for (int i = 0; i < n; ++i) r.max_bond = std::max<int64_t>(r.max_bond, rb[b][i]);
+      r.peak_entries = st.peak_entries;
+      r.seconds = secs;
+      r.flops_algorithmic = flops_inst[b];
+      r.rank_fallbacks = 0;
+      r.host_syncs = ctx->host_syncs;
+    }
+  }
+}
+
+void overlap_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* a, const ttn_s* const* bb, cplx* out) {
+  const ttn_s* ref = a[0];
+  for (int j = 0; j < nb; ++j) {
+    if (!a[j] || !bb[j]) throw Error(TTN_ERR_ARG, "NULL handle");
+    if (a[j]->kind != TTN_STATE || bb[j]->kind != TTN_STATE) throw Error(TTN_ERR_ARG, "ttn_overlap expects states");
+    if (a[j]->parent != ref->parent || bb[j]->parent != ref->parent) throw Error(TTN_ERR_TOPOLOGY, "topology mismatch");
+    if (a[j]->phys != ref->phys || bb[j]->phys != ref->phys) throw Error(TTN_ERR_SHAPE, "leg mismatch: physical dimensions");
+  }
+  const int n = ref->n;
+  int maxd = 0;
+  for (int i = 0; i < n; ++i) maxd = std::max(maxd, ref->depth[i]);
+  ctx->scratch.reset();
+  ctx->env.reset();
+  std::vector<Fac> E((size_t)nb * n);
+  ExecStats st;
+  for (int L = maxd; L >= 0; --L) {
+    std::vector<Task> tasks;
+    std::vector<Fac*> dst;
+    for (int j = 0; j < nb; ++j)
+      for (int i = 0; i < n; ++i) {
+        if (ref->depth[i] != L) continue;
+        Task t;
+        Operand A, B;
+        A.ptr = a[j]->node(i); A.dims = a[j]->shape[i]; A.conj = true;
+        B.ptr = bb[j]->node(i); B.dims = bb[j]->shape[i];
+        A.labels.push_back(L_SIG);
+        B.labels.push_back(L_SIG);
+        for (size_t l = 0; l + 1 < A.dims.size(); ++l) {
+          A.labels.push_back(L_A + (int)l);
+          B.labels.push_back(L_B + (int)l);
+        }
+        t.ops.push_back(A);
+        t.ops.push_back(B);
+        for (size_t l = 0; l < ref->children[i].size(); ++l) {
+          const Fac& ec = E[(size_t)j * n + ref->children[i][l]];
+          Operand F;
+          F.ptr = ec.p;
+          F.dims = {ec.a, ec.b};
+          F.labels = {L_A + 1 + (int)l, L_B + 1 + (int)l};
+          t.ops.push_back(F);
+        }
+        t.out_labels = {L_A, L_B};
+        Fac& e = E[(size_t)j * n + i];
+        e.a = A.dims[1];
+        e.b = B.dims[1];
+        e.k = 1;
+        e.p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * e.a * e.b));
+        t.out = e.p;
+        tasks.push_back(t);
+      }
+    contract_batch(ctx, tasks, st);
+    ctx->scratch.reset();
+  }
+  ctx->ensure_small(sizeof(cplx) * nb);
+  cplx* h = reinterpret_cast<cplx*>(ctx->hbuf);
+  for (int j = 0; j < nb; ++j)
+    TTN_CUDA(cudaMemcpyAsync(h + j, E[(size_t)j * n + ref->root].p, sizeof(cplx), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  TTN_CUDA(cudaGetLastError());
+  for (int j = 0; j < nb; ++j) out[j] = h[j];
+  ctx->env.reset();
+}
+
+}  // namespace tcbc

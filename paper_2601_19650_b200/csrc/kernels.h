@@ -1,0 +1,123 @@
+// Device-kernel launchers of libttncbc (grouped / batched problems, complex128).
+// Every launcher takes a host copy of the problem array (for scheduling) and a device copy
+// (what the kernel reads); both describe the same problems.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tcbc {
+
+typedef double2 cplx;   // (x = re, y = im), 16-byte aligned
+
+// op bits: bit0 = transpose, bit1 = conjugate
+enum { OP_N = 0, OP_T = 1, OP_R = 2 /*conj, no transpose*/, OP_C = 3 /*conj transpose*/ };
+
+// C[M,N] = alpha * op(A)[M,K] * op(B)[K,N] + beta * C.  Row-major storage:
+//   op(A) untransposed: A[m*lda + k];  transposed: A[k*lda + m]
+//   op(B) untransposed: B[k*ldb + n];  transposed: B[n*ldb + k]
+struct GemmProblem {
+  const cplx* A;
+  const cplx* B;
+  cplx* C;
+  long long lda, ldb, ldc;
+  int M, N, K;
+  int opA, opB;
+  int tile_start;      // filled by the launcher
+  int tiles_n;         // filled by the launcher
+  int pad_;
+  cplx alpha, beta;
+};
+
+// dst[i] = (conj?) src[offset(i)], dst contiguous with dims[0..rank) (row-major);
+// sstride[r] is the source stride of destination axis r.
+struct PermProblem {
+  const cplx* src;
+  cplx* dst;
+  long long total;
+  long long start;     // filled by the launcher (prefix of totals)
+  int rank;
+  int conj;
+  long long dims[8];
+  long long sstride[8];
+};
+
+// Top-kmax eigenpairs of an n x n Hermitian matrix A (full storage, row-major, lda = n;
+// destroyed).  Writes lam[0..kmax) descending, Vt[t*n + i] = i-th entry of eigenvector t,
+// and the truncation decision k = min(max_bond, #{lam > tol^2 lam_1}, #{lam > floor lam_1}) >= 1,
+// discarded weight w = trace - sum_{t<k} lam_t, trace, and zero-matrix flag.
+struct HeevProblem {
+  cplx* A;
+  int n;
+  int kmax;
+  double* lam;
+  cplx* Vt;
+  int* k_out;          // may be null
+  double* w_out;       // may be null
+  double* work;        // real workspace, heev_work_doubles(n) entries
+  cplx* tau;           // n entries
+  double tol2;         // tol^2
+  double floor_rel;    // rank floor on lam / lam_1
+  int max_bond;
+  int pad_;
+};
+size_t heev_work_doubles(int n, int kmax);
+size_t heev_smem_bytes(int n, int kmax);
+int heev_max_n();
+
+// In-place lower Cholesky A = L L^H of an n x n Hermitian matrix (full storage, ld = lda);
+// the strict upper triangle is zeroed.  info = 0 or j+1 at the first pivot <= rel_tol * max diag.
+struct PotrfProblem {
+  cplx* A;
+  long long lda;
+  int n;
+  int pad_;
+  int* info;
+  double rel_tol;
+};
+
+// Linv = L^{-1} (n x n lower, full storage, upper zeroed).
+struct TrtriProblem {
+  const cplx* L;
+  cplx* Linv;
+  long long ld;
+  int n;
+  int pad_;
+};
+
+// G-route factor F[t*ldf + c] = sqrt(max(lam_t,0)) * conj(Vt[t*n + c]), t < kmax, c < n.
+struct ScaleRowsProblem {
+  const cplx* Vt;
+  const double* lam;
+  cplx* F;
+  int kmax;
+  int n;
+  long long start;
+};
+
+// Copies a host array to device memory, stream-ordered before the next launch; the returned
+// device pointer stays valid until the owner's next host synchronisation.
+struct Stager {
+  virtual void* put(const void* host, size_t bytes) = 0;
+  virtual ~Stager() {}
+};
+
+// Launchers fill the scheduling fields of the host problems, stage them, and launch.
+void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_scale_rows(ScaleRowsProblem* h, int n, Stager& st, cudaStream_t s);
+// out[j] = sum_i |x_j[i]|^2 of n device vectors
+struct SumsqProblem { const cplx* x; long long len; double* out; };
+void launch_sumsq(SumsqProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_fill(cplx* p, long long n, cplx v, cudaStream_t s);
+// P[i*ld + j] = (i == j) for i < m, j < ncols, grouped
+struct EyeProblem { cplx* p; int m; int ncols; long long start; };
+void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s);
+
+// Counters of kernel launches issued by this library (for the bench's gpu_launches claim).
+long long launch_count();
+void count_launch();
+
+}  // namespace tcbc

@@ -1,0 +1,139 @@
+// Layout and reduction kernels of the CBC path (HBM-bound): grouped leg permutations
+// (ingest / egress and the operand reshapes between contraction steps), the eigenvector-row
+// scaling that forms the Gram-route factor L = Lambda^{1/2} V^H ("compressed ... via
+// singular value decomposition", reading A1/A2), Frobenius sums of squares for ||phi||.
+#include "kernels.h"
+#include <atomic>
+#include <algorithm>
+
+namespace tcbc {
+
+static std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1); }
+
+namespace {
+
+template <typename P>
+__device__ __forceinline__ int find_by_start(const P* p, int n, long long idx) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p[mid].start <= idx) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void permute_grouped(const PermProblem* __restrict__ probs, int nprob, long long total) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    int pi = find_by_start(probs, nprob, g);
+    const PermProblem& P = probs[pi];
+    long long i = g - P.start, rem = i, off = 0;
+    for (int r = P.rank - 1; r >= 0; --r) {
+      long long d = P.dims[r];
+      long long x = rem % d;
+      rem /= d;
+      off += x * P.sstride[r];
+    }
+    cplx v = P.src[off];
+    if (P.conj) v.y = -v.y;
+    P.dst[i] = v;
+  }
+}
+
+__global__ void scale_rows_grouped(const ScaleRowsProblem* __restrict__ probs, int nprob, long long total) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    int pi = find_by_start(probs, nprob, g);
+    const ScaleRowsProblem& P = probs[pi];
+    long long i = g - P.start;
+    int t = (int)(i / P.n), c = (int)(i % P.n);
+    double s = sqrt(fmax(P.lam[t], 0.0));
+    cplx v = P.Vt[(long long)t * P.n + c];
+    P.F[(long long)t * P.n + c] = make_double2(s * v.x, -s * v.y);
+  }
+}
+
+__global__ void sumsq_kernel(const SumsqProblem* __restrict__ probs) {
+  const SumsqProblem P = probs[blockIdx.x];
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < P.len; i += blockDim.x) {
+    cplx v = P.x[i];
+    acc += v.x * v.x + v.y * v.y;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) *P.out = acc;
+  }
+}
+
+__global__ void eye_grouped(const EyeProblem* __restrict__ probs, int nprob, long long total) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    int pi = find_by_start(probs, nprob, g);
+    const EyeProblem& P = probs[pi];
+    long long i = g - P.start;
+    long long r = i / P.ncols, c = i % P.ncols;
+    P.p[i] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+}
+
+__global__ void fill_kernel(cplx* p, long long n, cplx v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+int grid_for(long long total, int threads) {
+  long long b = (total + threads - 1) / threads;
+  return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 16));
+}
+
+}  // namespace
+
+void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s) {
+  long long total = 0;
+  for (int i = 0; i < n; ++i) { h[i].start = total; total += h[i].total; }
+  if (total == 0) return;
+  const PermProblem* d = static_cast<const PermProblem*>(st.put(h, sizeof(PermProblem) * n));
+  permute_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  count_launch();
+}
+
+void launch_scale_rows(ScaleRowsProblem* h, int n, Stager& st, cudaStream_t s) {
+  long long total = 0;
+  for (int i = 0; i < n; ++i) { h[i].start = total; total += (long long)h[i].kmax * h[i].n; }
+  if (total == 0) return;
+  const ScaleRowsProblem* d = static_cast<const ScaleRowsProblem*>(st.put(h, sizeof(ScaleRowsProblem) * n));
+  scale_rows_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  count_launch();
+}
+
+void launch_sumsq(SumsqProblem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  const SumsqProblem* d = static_cast<const SumsqProblem*>(st.put(h, sizeof(SumsqProblem) * n));
+  sumsq_kernel<<<n, 256, 0, s>>>(d);
+  count_launch();
+}
+
+void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s) {
+  long long total = 0;
+  for (int i = 0; i < n; ++i) { h[i].start = total; total += (long long)h[i].m * h[i].ncols; }
+  if (total == 0) return;
+  const EyeProblem* d = static_cast<const EyeProblem*>(st.put(h, sizeof(EyeProblem) * n));
+  eye_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  count_launch();
+}
+
+void launch_fill(cplx* p, long long n, cplx v, cudaStream_t s) {
+  if (n <= 0) return;
+  fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
+  count_launch();
+}
+
+}  // namespace tcbc

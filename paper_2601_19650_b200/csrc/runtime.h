@@ -1,0 +1,108 @@
+// Host runtime of libttncbc: context (device, stream, staging, arenas), TTN handles,
+// and the status plumbing behind the C ABI (include/ttn_cbc.h).
+#pragma once
+#include "../../include/ttn_cbc.h"
+#include "kernels.h"
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tcbc {
+
+// Error carried to the ABI boundary (converted to a ttn_status there).
+struct Error : std::runtime_error {
+  ttn_status status;
+  Error(ttn_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define TTN_CUDA(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e__ = (x);                                                                   \
+    if (e__ != cudaSuccess)                                                                  \
+      throw ::tcbc::Error(e__ == cudaErrorMemoryAllocation ? TTN_ERR_OOM : TTN_ERR_CUDA,      \
+                         std::string(#x) + ": " + cudaGetErrorString(e__));                  \
+  } while (0)
+
+// Bump allocator over device chunks.  reset() recycles the memory for later work on the
+// SAME stream (stream order makes the reuse safe without a host sync).
+class Arena {
+ public:
+  explicit Arena(size_t chunk = 256ull << 20) : chunk_(chunk) {}
+  ~Arena();
+  void* alloc(size_t bytes);
+  void reset();
+  void release();
+  size_t high_water() const { return high_; }
+
+ private:
+  struct Chunk { char* p; size_t size; size_t used; };
+  std::vector<Chunk> chunks_;
+  size_t cur_ = 0, chunk_, high_ = 0, live_ = 0;
+};
+
+// Pinned host ring mirrored in device memory; put() enqueues one H2D copy.
+class RingStager : public Stager {
+ public:
+  RingStager(cudaStream_t s, size_t bytes = 64ull << 20);
+  ~RingStager();
+  void* put(const void* host, size_t bytes) override;
+  void epoch();   // call after a stream synchronisation: the whole ring is free again
+ private:
+  cudaStream_t s_;
+  char* h_ = nullptr;
+  char* d_ = nullptr;
+  size_t size_, off_ = 0;
+};
+
+}  // namespace tcbc
+
+struct ttn_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  tcbc::RingStager* stager = nullptr;
+  tcbc::Arena scratch;      // per-stage temporaries (reset between stages)
+  tcbc::Arena env;          // per-apply environment factors (reset per apply)
+  // pinned host buffer for small D2H reads (ranks, weights, norms)
+  char* hbuf = nullptr;
+  size_t hbuf_size = 0;
+  char* dbuf = nullptr;    // device mirror of small results
+  size_t dbuf_size = 0;
+  int host_syncs = 0;
+  void sync();             // cudaStreamSynchronize + stager epoch
+  void ensure_small(size_t bytes);
+};
+
+struct ttn_s {
+  ttn_ctx_s* ctx = nullptr;
+  int kind = TTN_STATE;
+  int n = 0;
+  int root = -1;
+  std::vector<int> parent, phys;
+  std::vector<int64_t> bond;
+  std::vector<std::vector<int>> children;
+  std::vector<int> depth;
+  std::vector<std::vector<int64_t>> shape;
+  std::vector<int64_t> offset;   // element offset of node i in data
+  int64_t total = 0;
+  tcbc::cplx* data = nullptr;     // one device allocation (cudaMallocAsync)
+  tcbc::cplx* node(int i) const { return data + offset[i]; }
+};
+
+namespace tcbc {
+
+// Topology helpers shared by create / apply / overlap.
+void build_topology(ttn_s* t, const int32_t* parent, int n);
+void finalize_shapes(ttn_s* t);   // shapes / offsets / total from kind, phys, bond
+ttn_s* new_ttn_like(ttn_ctx_s* ctx, const ttn_s* tmpl, int kind, const std::vector<int64_t>& bond);
+void free_ttn(ttn_s* t);
+
+// Batched drivers (cbc.cpp)
+void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts,
+                    int64_t max_bond, double tol, ttn_s** outs, ttn_cbc_report* reps);
+void overlap_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* a, const ttn_s* const* b, cplx* out);
+
+}  // namespace tcbc

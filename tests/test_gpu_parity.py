@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on identical seeded inputs.
+
+Tolerances (B:5): gauge-invariant 1 - Re<phi_gpu|phi_oracle>/(|.||.|) <= 1e-10 and the
+truncation error eps^2 = 1 - |phi|^2/|O psi|^2 within 1e-10 of the oracle's; untruncated
+runs also match the dense O|psi> to 1e-12 relative (P1).  Ranks must be identical.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import TTN, cbc_apply as oracle_cbc, exact_apply, norm, overlap, to_dense_operator, to_dense_state
+
+from ._helpers import distances, gpu_pair, oracle_pair, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_19650_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def _run(P, ctx, inst, max_bond=None, tol=0.0):
+    mb = inst.max_bond if max_bond is None else max_bond
+    op_g, st_g = gpu_pair(P, ctx, inst)
+    out, rep = P.cbc_apply(ctx, op_g, st_g, mb, tol)
+    phi_g = to_oracle(P, out, inst.parent)
+    op_o, psi_o = oracle_pair(inst)
+    phi_o = oracle_cbc(op_o, psi_o, mb, tol)
+    return phi_g, phi_o, rep, op_o, psi_o
+
+
+def _check(phi_g, phi_o, op_o, psi_o, rep, bonds=True):
+    d_cos, d_rel = distances(phi_g, phi_o)
+    assert d_cos <= 1e-10, (d_cos, d_rel)
+    on2 = norm(exact_apply(op_o, psi_o)) ** 2
+    e_g = 1 - norm(phi_g) ** 2 / on2
+    e_o = 1 - norm(phi_o) ** 2 / on2
+    assert abs(e_g - e_o) <= 1e-10, (e_g, e_o)
+    assert abs(rep["norm"] - norm(phi_o)) <= 1e-10 * norm(phi_o)
+    if bonds:
+        assert phi_g.bonds() == phi_o.bonds()
+    for i, t in enumerate(phi_g.tensors):       # P3 on the GPU output
+        if i == phi_g.root:
+            continue
+        q = np.moveaxis(t, 1, -1).reshape(-1, t.shape[1])
+        assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
+
+
+def test_overlap_and_norm_match_oracle(P, ctx):
+    for k, seed in ((1, 0), (3, 1)):
+        inst = W.make_config(k, seed=seed)
+        inst2 = W.make_config(k, seed=seed + 10)
+        a = P.ttn_create(ctx, P.TTN_STATE, inst.parent, inst.phys, inst.state_bond, inst.state)
+        b = P.ttn_create(ctx, P.TTN_STATE, inst2.parent, inst2.phys, inst2.state_bond, inst2.state)
+        A, B = TTN(inst.parent, inst.state), TTN(inst2.parent, inst2.state)
+        ref = overlap(A, B)
+        got = P.ttn_overlap(ctx, a, b)
+        assert abs(got - ref) <= 1e-13 * norm(A) * norm(B)
+        assert abs(P.ttn_norm(ctx, a) - norm(A)) <= 1e-13 * norm(A)
+
+
+def test_roundtrip_tensors(P, ctx):
+    inst = W.make_config(3, seed=2)
+    h = P.ttn_create(ctx, P.TTN_STATE, inst.parent, inst.phys, inst.state_bond, inst.state)
+    for i in (0, 5, 30):
+        assert np.array_equal(h.get(i), inst.state[i])
+
+
+def test_config1_untruncated_matches_dense(P, ctx):
+    inst = W.make_config(1, max_bond=12)
+    phi_g, phi_o, rep, op_o, psi_o = _run(P, ctx, inst)
+    ex = to_dense_operator(op_o) @ to_dense_state(psi_o)
+    v = to_dense_state(phi_g)
+    assert np.linalg.norm(v - ex) <= 1e-12 * np.linalg.norm(ex)
+    assert phi_g.bonds() == [1, 2, 4, 8, 4, 2]
+
+
+def test_config1_truncated(P, ctx):
+    inst = W.make_config(1, max_bond=6)
+    phi_g, phi_o, rep, op_o, psi_o = _run(P, ctx, inst)
+    _check(phi_g, phi_o, op_o, psi_o, rep)
+
+
+SMALL = [
+    ("binary7", W.complete_binary(7), 3, 2, [64, 3]),
+    ("binary15", W.complete_binary(15), 4, 3, [64, 5]),
+    ("star", W.star_of_chains_literal(3, 2), 3, 2, [64, 4]),
+    ("ttree", W.t_tree(3), 4, 3, [64, 4]),
+    ("ftps", W.ftps(2), 3, 2, [64, 3]),
+    ("chain9", W.chain(9), 5, 3, [64, 7]),
+]
+
+
+@pytest.mark.parametrize("name,parent,chi,D,mbs", SMALL)
+def test_small_trees(P, ctx, name, parent, chi, D, mbs):
+    for mb in mbs:
+        inst = W.configs.random_instance(parent, [2] * len(parent), chi, D, mb, seed=7)
+        phi_g, phi_o, rep, op_o, psi_o = _run(P, ctx, inst)
+        _check(phi_g, phi_o, op_o, psi_o, rep)
+        if mb == 64:
+            ex = to_dense_operator(op_o) @ to_dense_state(psi_o)
+            v = to_dense_state(phi_g)
+            assert np.linalg.norm(v - ex) <= 1e-12 * np.linalg.norm(ex)
+
+
+def test_mixed_physical_dims(P, ctx):
+    parent = W.complete_binary(7)
+    phys = [1, 2, 3, 2, 1, 2, 3]
+    inst = W.configs.random_instance(parent, phys, 3, 2, 4, seed=9)
+    phi_g, phi_o, rep, op_o, psi_o = _run(P, ctx, inst)
+    _check(phi_g, phi_o, op_o, psi_o, rep)
+
+
+def test_tolerance_truncation(P, ctx):
+    inst = W.make_config(1, max_bond=12)
+    for tol in (0.3, 0.05):
+        phi_g, phi_o, rep, op_o, psi_o = _run(P, ctx, inst, tol=tol)
+        _check(phi_g, phi_o, op_o, psi_o, rep)
+
+
+def test_config2_full(P, ctx):
+    inst = W.make_config(2)
+    phi_g, phi_o, rep, op_o, psi_o = _run(P, ctx, inst)
+    _check(phi_g, phi_o, op_o, psi_o, rep)
+
+
+def test_config3_batch_matches_oracle(P, ctx):
+    seeds = [0, 1, 2, 3]
+    insts = [W.make_config(3, seed=s) for s in seeds]
+    pairs = [gpu_pair(P, ctx, i) for i in insts]
+    outs, reps = P.cbc_apply_batch(ctx, [p[0] for p in pairs], [p[1] for p in pairs], 32)
+    for inst, out, rep in zip(insts, outs, reps):
+        op_o, psi_o = oracle_pair(inst)
+        phi_o = oracle_cbc(op_o, psi_o, 32)
+        _check(to_oracle(P, out, inst.parent), phi_o, op_o, psi_o, rep)
+
+
+def test_errors(P, ctx):
+    inst = W.make_config(1)
+    op, st = gpu_pair(P, ctx, inst)
+    with pytest.raises(P.TTNError):
+        P.cbc_apply(ctx, op, st, 0)
+    with pytest.raises(P.TTNError):
+        P.cbc_apply(ctx, st, op, 4)
+    other = W.make_config(3)
+    op3, st3 = gpu_pair(P, ctx, other)
+    with pytest.raises(P.TTNError) as e:
+        P.cbc_apply(ctx, op3, st, 4)
+    assert "TOPOLOGY" in str(e.value)
+    with pytest.raises(P.TTNError):
+        P.ttn_create(ctx, P.TTN_STATE, [-1, -1], [2, 2], [1, 1], [np.zeros((2, 1)), np.zeros((2, 1))])
+
+
+def test_zero_state(P, ctx):
+    inst = W.make_config(1, max_bond=6)
+    op, _ = gpu_pair(P, ctx, inst)
+    z = P.ttn_create(ctx, P.TTN_STATE, inst.parent, inst.phys, inst.state_bond, [t * 0 for t in inst.state])
+    out, rep = P.cbc_apply(ctx, op, z, 6)
+    assert out.bonds() == [1] * 6
+    assert rep["norm"] == 0.0
