@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""CBC TTNO.TTNS applies/sec and FP64 TFLOP/s on B200 (BASELINE.json metric, B:2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl native|reference]
+
+Workload (config.workload): BASELINE config 3 by default (B:9) — 64 independent complete-
+binary TTNs (31 nodes, d=2, chi=32, D=6) per GPU, max_bond 32, seeds rank*64 + 0..63.  A step
+is one cbc_apply_batch over the 64 instances (the whole hot path: up-sweep, down-sweep,
+compressions, final sweep, assembly).  Multi-GPU: one process per GPU (torchrun), each with
+its own 64 instances, no data-path collective ("scaling": "weak"); timing is the max over
+ranks of the CUDA-event time on the library's stream.  --config 2 (single 32-site MPO.MPS,
+replicas) and --config 5 (63-qubit circuit, a step = 10 layers x 64 seeds) are also available.
+
+The oracle (oracle/) is executed only by the cpu_baseline leg (rank 0, N=1) and by
+--impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+FP64_PEAK_TFLOPS = 37.1      # measured DMMA m8n8k4 peak on this pool (profiles/fp64_peaks_r01.json)
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA loop on B200 (profiles/fp64_peaks_r01.json); MEASURED_PEAKS.json has no FP64 entry"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 5])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="short run for ncu: no e2e/cpu/clocks")
+    return ap.parse_args()
+
+
+def workload_desc(cfg, batch):
+    c = W.CONFIGS[cfg]
+    if cfg == 3:
+        return {"workload": f"BASELINE config 3: {batch} independent complete-binary TTNs (31 nodes, d=2 every node, "
+                            "chi=32, D=6), complex128 Gaussian, max_bond=32", "batch_per_gpu": batch,
+                "l2": "inputs larger than L2 (0.94 GB per GPU per step)"}
+    if cfg == 2:
+        return {"workload": "BASELINE config 2: MPO.MPS chain N=32, d=2, chi=64, D=8, max_bond=64, single instance",
+                "batch_per_gpu": batch, "l2": "inputs (3.9 MB) fit in L2: L2 flushed between steps"}
+    if cfg == 5:
+        return {"workload": f"BASELINE config 5: 63-qubit binary-tree circuit from |0..0>, 10 layers of Haar 2-qubit "
+                            f"gates on seeded matchings, max_bond=256, {batch} seeds; a step = 10 layers x {batch} seeds",
+                "batch_per_gpu": batch, "l2": "L2 flushed between steps"}
+    return {"workload": f"BASELINE config {cfg}", "batch_per_gpu": batch}
+
+
+def make_instances(cfg, seeds):
+    return [W.make_config(cfg, seed=s) for s in seeds]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.p = None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self, gpu_index):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9 or parts[0] != str(gpu_index):
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_time(cfg, seeds, reps=1):
+    """Time the oracle as it stands on this host (test infrastructure; the only bench use)."""
+    import oracle as O
+    insts = make_instances(cfg, seeds)
+    pairs = []
+    for inst in insts:
+        psi = O.TTN(inst.parent, [t.copy() for t in inst.state])
+        psi.tensors[psi.root] = psi.tensors[psi.root] / O.norm(psi)
+        pairs.append((O.TTN(inst.parent, inst.op, "operator"), psi, inst))
+    t0 = time.perf_counter()
+    napply = 0
+    for _ in range(reps):
+        for op, psi, inst in pairs:
+            if cfg == 5:
+                st = psi
+                for layer in range(inst.layers):
+                    ops, _, _ = W.circuit_layer_operator(inst.parent, inst.seed, layer)
+                    st = O.cbc_apply(O.TTN(inst.parent, ops, "operator"), st, inst.max_bond)
+                    napply += 1
+            else:
+                O.cbc_apply(op, psi, inst.max_bond)
+                napply += 1
+    return napply, time.perf_counter() - t0
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg):
+    sample = {3: [1000 + i for i in range(10)], 2: [0, 1], 5: [1000, 1001, 1002, 1003], 1: list(range(50))}[cfg]
+    n, dt = oracle_time(cfg, sample)
+    unit = "applies/s"
+    return {"value": n / dt, "unit": unit, "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{len(sample)} instances of config {cfg} ({n} applies, seeds {sample[0]}..{sample[-1]}), "
+                      f"NumPy/LAPACK oracle as it stands, {dt:.1f} s on {os.cpu_count()} host cores"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = args.config
+    per_step = {3: 2, 2: 1, 5: 1, 1: 20}[cfg]
+    for w in range(args.warmup):
+        oracle_time(cfg, [2000 + w * per_step + i for i in range(per_step)])
+    times, napp = [], 0
+    for k in range(args.steps):
+        n, dt = oracle_time(cfg, [3000 + k * per_step + i for i in range(per_step)])
+        times.append(dt)
+        napp += n
+    tot = sum(times)
+    value = napp / tot
+    batch = args.batch or {3: 64, 2: 1, 5: 64, 1: 1}[cfg]
+    line = {"metric": "CBC TTNO.TTNS applies/sec (FP64)", "value": value, "unit": "applies/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic", "config": workload_desc(cfg, batch),
+            "cpu_baseline": {"value": value, "unit": "applies/s", "cores": blas_threads(), "kind": "oracle",
+                             "sample": f"each step = {per_step} instance(s) of config {cfg} on the host CPU "
+                                       f"(NumPy/LAPACK oracle, {os.cpu_count()} cores)"},
+            "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- native arm
+def run_native(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2601_19650_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    cfg = args.config
+    batch = args.batch or {3: 64, 2: 1, 5: 64, 1: 1}[cfg]
+    seeds = [rank * batch + i for i in range(batch)]
+    insts = make_instances(cfg, seeds)
+    stream = torch.cuda.Stream(local_rank)
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(local_rank, stream.cuda_stream)
+    mb = insts[0].max_bond
+    parent, phys = insts[0].parent, insts[0].phys
+
+    # inputs: normalised on the GPU (A16), then resident in HBM for the device-timed loop
+    states, host_states = [], []
+    for inst in insts:
+        h = P.ttn_create(ctx, P.TTN_STATE, inst.parent, inst.phys, inst.state_bond, inst.state)
+        nrm = P.ttn_norm(ctx, h)
+        h.destroy()
+        tens = [t.copy() for t in inst.state]
+        r = inst.parent.index(-1)
+        tens[r] = tens[r] / nrm
+        host_states.append(tens)
+        states.append(P.ttn_create(ctx, P.TTN_STATE, inst.parent, inst.phys, inst.state_bond, tens))
+    if cfg == 5:
+        layer_ops = []
+        for layer in range(insts[0].layers):
+            ops = []
+            for inst in insts:
+                o, ob, _ = W.circuit_layer_operator(inst.parent, inst.seed, layer)
+                ops.append((o, ob))
+            layer_ops.append(ops)
+        dev_layers = [[P.ttn_create(ctx, P.TTN_OPERATOR, parent, phys, ob, o) for (o, ob) in ops] for ops in layer_ops]
+    else:
+        ops = [P.ttn_create(ctx, P.TTN_OPERATOR, i.parent, i.phys, i.op_bond, i.op) for i in insts]
+
+    flush = None
+    if cfg in (2, 5):
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local_rank}")
+
+    def step():
+        """One pass of the hot path over the batch; returns (applies, flops)."""
+        if cfg == 5:
+            cur = states
+            fl = 0.0
+            for layer in range(len(dev_layers)):
+                nxt, reps = P.cbc_apply_batch(ctx, dev_layers[layer], cur, mb)
+                fl += sum(r["flops_algorithmic"] for r in reps)
+                if cur is not states:
+                    for h in cur:
+                        h.destroy()
+                cur = nxt
+            for h in cur:
+                h.destroy()
+            return batch * len(dev_layers), fl
+        outs, reps = P.cbc_apply_batch(ctx, ops, states, mb)
+        for h in outs:
+            h.destroy()
+        return batch, sum(r["flops_algorithmic"] for r in reps)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")) if not args.quick else None
+    if clocks:
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        clocks.start()
+        time.sleep(0.3)
+    P.ttn_profile_enable(True)
+    lc0 = P.ttn_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total, applies, flops = 0.0, 0, 0.0
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        a, f = step()
+        e1.record(stream)
+        e1.synchronize()
+        ms_total += e0.elapsed_time(e1)
+        applies += a
+        flops += f
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = P.ttn_launch_count() - lc0
+    prof = {fam: P.ttn_profile_read(fam) for fam in ("all", "zgemm", "heev", "potrf", "trtri", "geqr", "permute",
+                                                     "scale_rows", "misc")}
+    P.ttn_profile_enable(False)
+    clk = clocks.stop(local_rank) if clocks else None
+
+    t = torch.tensor([ms_total, flops, float(applies)], dtype=torch.float64, device=f"cuda:{local_rank}")
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, flops_all, applies_all = mx[0].item(), sm[1].item(), sm[2].item()
+    else:
+        ms_max, flops_all, applies_all = ms_total, flops, float(applies)
+
+    # ------------------------------------------------------------------ e2e (host buffers)
+    e2e = None
+    if not args.no_e2e and not args.quick and cfg != 5:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_states = [[pin(t) for t in ts] for ts in host_states]
+        h_ops = [[pin(t) for t in i.op] for i in insts]
+        h2d = sum(t.numel() * 16 for ts in h_states for t in ts) + sum(t.numel() * 16 for ts in h_ops for t in ts)
+        n_e2e = max(1, min(3, args.steps))
+        out_bufs = None
+        d2h = 0
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            st_h = [P.ttn_create(ctx, P.TTN_STATE, parent, phys, i.state_bond, ts) for i, ts in zip(insts, h_states)]
+            op_h = [P.ttn_create(ctx, P.TTN_OPERATOR, parent, phys, i.op_bond, ts) for i, ts in zip(insts, h_ops)]
+            outs, reps = P.cbc_apply_batch(ctx, op_h, st_h, mb)
+            if out_bufs is None:
+                out_bufs = []
+                for o in outs:
+                    tot = sum(int(np.prod(o.shape(j))) for j in range(o.n_nodes))
+                    out_bufs.append(torch.empty(tot, dtype=torch.complex128).pin_memory())
+                d2h = sum(b.numel() * 16 for b in out_bufs)
+            for o, b in zip(outs, out_bufs):
+                P.ttn_get_data(ctx, o, b)
+            for h in st_h + op_h + outs:
+                h.destroy()
+        e1.record(stream)
+        e1.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local_rank}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": batch * world * n_e2e / (te.item() / 1000.0), "unit": "applies/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "note": "ttn_create from pinned host buffers + cbc_apply_batch + ttn_get_data, CUDA events, max over ranks"}
+
+    if rank != 0:
+        ctx.close()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and not args.quick:
+        cpu = cpu_baseline(cfg)
+    g = prof["zgemm"]
+    ach = g["flops"] / (g["ms"] / 1000.0) / 1e12 if g["ms"] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_zgemm_traffic_r01.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    value = applies_all / (ms_max / 1000.0)
+    kern = {k: {"ms": v["ms"], "share_of_kernel_time": v["ms"] / prof["all"]["ms"] if prof["all"]["ms"] else None,
+                "launches": v["launches"], "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 else None}
+            for k, v in prof.items() if v["launches"]}
+    line = {
+        "metric": "CBC TTNO.TTNS applies/sec (FP64)",
+        "value": value,
+        "unit": "applies/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128 (f64)",
+        "data": "synthetic",
+        "config": dict(workload_desc(cfg, batch), parallelism=f"instance-sharded x{world}"),
+        "fp64_tflops_end_to_end": flops_all / (ms_max / 1000.0) / 1e12,
+        "fp64_frac_of_peak_end_to_end": flops_all / (ms_max / 1000.0) / 1e12 / FP64_PEAK_TFLOPS,
+        "roofline": {"bound": "tensor", "kernel": "zgemm_grouped (DMMA.8x8x4 complex GEMM)", "achieved": ach,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "peak_source": FP64_PEAK_SOURCE,
+                     "flops_per_launch": g["flops"] / max(g["launches"], 1),
+                     "ms_per_launch": g["ms"] / max(g["launches"], 1)},
+        "kernels": kern,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    run_native(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

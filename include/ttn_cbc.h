@@ -101,6 +101,10 @@ TTN_API ttn_status ttn_node_shape(ttn t, int32_t node, int32_t* ndim, int64_t* d
  * `capacity_elems` complex entries (ARG if too small).  Synchronises the ctx stream.    */
 TTN_API ttn_status ttn_get_tensor(ttn_ctx ctx, ttn t, int32_t node, ttn_c128* host_out, size_t capacity_elems);
 
+/* Copy every node (node 0 first, each in ABI leg order, concatenated) to host memory with
+ * one D2H copy; capacity_elems must cover the sum of the node sizes.  Synchronises.     */
+TTN_API ttn_status ttn_get_data(ttn_ctx ctx, ttn t, ttn_c128* host_out, size_t capacity_elems);
+
 /* ---------------------------------------------------------------- CBC                  */
 /* phi ~= O |psi> by CBC (§III.B, Eqs. 10-14; tensor train §III.A,
  * Eqs. 5-9, is the special case of a chain rooted at site 0).
@@ -125,6 +129,18 @@ TTN_API ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const
 TTN_API ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out);
 /* Batched overlaps <a_j|b_j>, j < n.                                                      */
 TTN_API ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b, ttn_c128* out);
+/* ---------------------------------------------------------------- measurement          */
+/* Process-wide kernel-family timing with CUDA events on the launching stream (used by
+ * bench.py for the roofline).  on = 1 resets and enables, 0 disables.                    */
+TTN_API ttn_status ttn_profile_enable(int on);
+/* Totals since enable for one family ("zgemm", "heev", "potrf", "trtri", "geqr", "permute",
+ * "scale_rows", "misc", or "all"): summed event time (ms), algorithmic flops and bytes of the
+ * launches, and the number of launches.  Synchronises the recorded events.              */
+TTN_API ttn_status ttn_profile_read(const char* family, double* ms, double* flops, double* bytes,
+                                    int64_t* launches);
+/* Number of kernels this library has launched in this process.                           */
+TTN_API ttn_status ttn_launch_count(int64_t* out);
+
 /* sqrt(Re <a|a>).                                                                         */
 TTN_API ttn_status ttn_norm(ttn_ctx ctx, ttn a, double* out);
 

@@ -67,9 +67,9 @@ class TTN:
         self.ctx, self.h, self.kind = ctx, h, kind
 
     def destroy(self):
-        if self.h:
+        if self.h and self.ctx.h:      # a handle outliving its context is not freed (ctx owns the pool)
             L.load().ttn_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
@@ -112,7 +112,7 @@ def ttn_create(ctx: Context, kind: int, parent: Sequence[int], phys: Sequence[in
             import torch
             assert t.dtype == torch.complex128 and t.is_contiguous()
             ptrs[i] = t.data_ptr()
-            dev = True if dev is None else dev
+            dev = bool(t.is_cuda) if dev is None else dev
             keep.append(t)
         else:
             a = L.host_c128(t)
@@ -129,6 +129,18 @@ def ttn_get_tensor(ctx: Context, t: TTN, node: int) -> np.ndarray:
     shp = t.shape(node)
     out = np.empty(shp, dtype=np.complex128)
     L.check(ctx.h, L.load().ttn_get_tensor(ctx.h, t.h, node, C.c_void_p(out.ctypes.data), out.size))
+    return out
+
+
+def ttn_get_data(ctx: Context, t: TTN, out=None):
+    """All nodes concatenated (node order, ABI leg order) into `out` (numpy complex128 or a
+    pinned torch complex128 CPU tensor); one D2H copy."""
+    total = sum(int(np.prod(t.shape(i))) for i in range(t.n_nodes))
+    if out is None:
+        out = np.empty(total, dtype=np.complex128)
+    ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+    cap = out.numel() if hasattr(out, "numel") else out.size
+    L.check(ctx.h, L.load().ttn_get_data(ctx.h, t.h, C.c_void_p(ptr), cap))
     return out
 
 
@@ -163,6 +175,22 @@ def ttn_overlap_batch(ctx: Context, a: Sequence[TTN], b: Sequence[TTN]) -> List[
     out = (L.c128 * n)()
     L.check(ctx.h, L.load().ttn_overlap_batch(ctx.h, n, pa, pb, out))
     return [complex(out[i].re, out[i].im) for i in range(n)]
+
+
+def ttn_profile_enable(on: bool = True) -> None:
+    L.check(None, L.load().ttn_profile_enable(int(bool(on))))
+
+
+def ttn_profile_read(family: str = "all") -> dict:
+    ms, fl, by, n = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+    L.check(None, L.load().ttn_profile_read(family.encode(), C.byref(ms), C.byref(fl), C.byref(by), C.byref(n)))
+    return {"ms": ms.value, "flops": fl.value, "bytes": by.value, "launches": n.value}
+
+
+def ttn_launch_count() -> int:
+    v = C.c_int64()
+    L.check(None, L.load().ttn_launch_count(C.byref(v)))
+    return v.value
 
 
 def ttn_norm(ctx: Context, a: TTN) -> float:

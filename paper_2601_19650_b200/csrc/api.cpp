@@ -1,7 +1,9 @@
 // extern "C" entry points of libttncbc (include/ttn_cbc.h).  Every call converts
 // exceptions to a ttn_status and records the message on the context.
+#include "prof.h"
 #include "runtime.h"
 
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -167,6 +169,16 @@ ttn_status ttn_get_tensor(ttn_ctx ctx, ttn t, int32_t node, ttn_c128* host_out, 
   });
 }
 
+ttn_status ttn_get_data(ttn_ctx ctx, ttn t, ttn_c128* host_out, size_t capacity_elems) {
+  if (!ctx || !t || !host_out) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    if ((size_t)t->total > capacity_elems) throw Error(TTN_ERR_ARG, "output buffer too small");
+    TTN_CUDA(cudaMemcpyAsync(host_out, t->data, sizeof(cplx) * t->total, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
 ttn_status cbc_apply(ttn_ctx ctx, ttn op, ttn state, int64_t max_bond, double tol, ttn* out, ttn_cbc_report* rep) {
   if (!ctx || !out) return TTN_ERR_ARG;
   return cbc_apply_batch(ctx, 1, &op, &state, max_bond, tol, out, rep);
@@ -203,6 +215,25 @@ ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b,
 }
 
 ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out) { return ttn_overlap_batch(ctx, 1, &a, &b, out); }
+
+ttn_status ttn_profile_enable(int on) {
+  prof_enable(on != 0);
+  return TTN_OK;
+}
+
+ttn_status ttn_profile_read(const char* family, double* ms, double* flops, double* bytes, int64_t* launches) {
+  if (!family || !ms || !flops || !bytes || !launches) return TTN_ERR_ARG;
+  long long l = 0;
+  prof_read(family, ms, flops, bytes, &l);
+  *launches = l;
+  return TTN_OK;
+}
+
+ttn_status ttn_launch_count(int64_t* out) {
+  if (!out) return TTN_ERR_ARG;
+  *out = launch_count();
+  return TTN_OK;
+}
 
 ttn_status ttn_norm(ttn_ctx ctx, ttn a, double* out) {
   if (!out) return TTN_ERR_ARG;

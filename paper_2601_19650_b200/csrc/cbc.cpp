@@ -172,7 +172,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
 }
 
 // CholeskyQR2 of every S (m > kd); Q = I for m <= kd.  Synchronises once for pivot flags.
-int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vector<double>& flops_inst) {
+int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vector<double>& flops_inst,
+             std::vector<int>& fb_inst) {
   if (jobs.empty()) return 0;
   std::vector<EyeProblem> eyes;
   std::vector<GemmProblem> g1, g2, g3, g4;
@@ -227,13 +228,18 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
   int* hi = reinterpret_cast<int*>(ctx->hbuf);
   TTN_CUDA(cudaMemcpyAsync(hi, d_info, sizeof(int) * 2 * jobs.size(), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();
-  int fails = 0;
+  // rank-deficient (or too ill-conditioned) S: Householder QR fallback, stream-ordered
+  std::vector<GeqrProblem> fb;
   for (int j : tall)
-    if (hi[2 * j] != 0 || hi[2 * j + 1] != 0) ++fails;
-  if (fails)
-    throw Error(TTN_ERR_NUMERIC, "CholeskyQR2 of S (Eq. 13) hit a non-positive pivot in " + std::to_string(fails) +
-                                     " node(s): rank-deficient S (fallback not available in this build)");
-  return 0;
+    if (hi[2 * j] != 0 || hi[2 * j + 1] != 0) {
+      QRJob& J = jobs[j];
+      cplx* tau = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * J.kd));
+      fb.push_back(GeqrProblem{const_cast<cplx*>(J.S), J.Q, tau, (int)J.m, (int)J.kd});
+      flops_inst[J.inst] += 8.0 * 2.0 * (double)J.m * J.kd * J.kd;
+      fb_inst[J.inst] += 1;
+    }
+  if (!fb.empty()) launch_geqr_q(fb.data(), (int)fb.size(), *ctx->stager, ctx->stream);
+  return (int)fb.size();
 }
 
 }  // namespace
@@ -276,6 +282,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   ctx->host_syncs = 0;
   ExecStats st;
   std::vector<double> w_inst(nb, 0.0), flops_inst(nb, 0.0);
+  std::vector<int> fb_inst(nb, 0);
   std::vector<Fac> up((size_t)nb * n), down((size_t)nb * n), R((size_t)nb * n);
   // trivial factor L^{[(-,r)]} = 1 (extent-1 legs)
   cplx* one = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx)));
@@ -427,7 +434,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       flops_inst[b] += 8.0 * (double)r * nz * ms;
     }
     gemm_batch(ctx, sg, st);
-    qr_batch(ctx, qj, st, flops_inst);
+    qr_batch(ctx, qj, st, flops_inst, fb_inst);
     if (!pq.empty()) launch_permute(pq.data(), (int)pq.size(), *ctx->stager, ctx->stream);
     gemm_batch(ctx, rg, st);
     ctx->scratch.reset();
@@ -450,6 +457,8 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   TTN_CUDA(cudaGetLastError());
   ctx->scratch.reset();
   ctx->env.reset();
+  for (int b = 0; b < nb; ++b)
+    if (!std::isfinite(hs[b])) throw Error(TTN_ERR_NUMERIC, "non-finite result (non-finite input?)");
   double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (reps) {
     for (int b = 0; b < nb; ++b) {
@@ -461,7 +470,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       r.peak_entries = st.peak_entries;
       r.seconds = secs;
       r.flops_algorithmic = flops_inst[b];
-      r.rank_fallbacks = 0;
+      r.rank_fallbacks = fb_inst[b];
       r.host_syncs = ctx->host_syncs;
     }
   }

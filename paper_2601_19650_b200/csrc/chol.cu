@@ -9,6 +9,7 @@
 // One CTA per matrix; right-looking column algorithm with the trailing Hermitian update
 // spread over the CTA.
 #include "kernels.h"
+#include "prof.h"
 #include <cmath>
 
 namespace tcbc {
@@ -106,19 +107,146 @@ __global__ void __launch_bounds__(256) trtri_grouped(const TrtriProblem* __restr
   }
 }
 
+// Householder QR (zgeqr2) of a tall m x k matrix A (row-major, ld k; destroyed) and the
+// thin Q = H_0 ... H_{k-1} [I; 0] written to Q (ld k).  Used for the S of Eq. 13 when
+// CholeskyQR2 flags a rank-deficient S (circuit layers, zero states): Householder gives an
+// isometry Q spanning range(S) for any rank, as the oracle's LAPACK QR does.
+__global__ void __launch_bounds__(256) geqr_q_grouped(const GeqrProblem* __restrict__ probs) {
+  const GeqrProblem P = probs[blockIdx.x];
+  const int m = P.m, k = P.k;
+  cplx* A = P.A;
+  cplx* Q = P.Q;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double red[32];
+  __shared__ cplx cred[8][33];
+  __shared__ cplx s_w[32];
+  for (int j = 0; j < k; ++j) {
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < m; i += 256) {
+      cplx x = A[(size_t)i * k + j];
+      part += x.x * x.x + x.y * x.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    double xn2 = 0.0;
+    for (int w = 0; w < 8; ++w) xn2 += red[w];
+    const cplx alpha = A[(size_t)j * k + j];
+    cplx tau = make_double2(0.0, 0.0), scale = make_double2(0.0, 0.0);
+    if (!(xn2 == 0.0 && alpha.y == 0.0)) {
+      const double beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn2), alpha.x);
+      tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+      const cplx den = make_double2(alpha.x - beta, alpha.y);
+      const double dd = den.x * den.x + den.y * den.y;
+      scale = make_double2(den.x / dd, -den.y / dd);
+    }
+    __syncthreads();
+    if (tid == 0) P.tau[j] = tau;
+    for (int i = j + 1 + tid; i < m; i += 256) A[(size_t)i * k + j] = cmul(A[(size_t)i * k + j], scale);
+    if (tid == 0) A[(size_t)j * k + j] = make_double2(1.0, 0.0);   // v_j = 1 (R_jj not needed)
+    __syncthreads();
+    if (tau.x == 0.0 && tau.y == 0.0) continue;
+    const cplx ctau = make_double2(tau.x, -tau.y);
+    for (int c0 = j + 1; c0 < k; c0 += 32) {   // A[j:, j+1:] -= conj(tau) v (v^H A)
+      const int c = c0 + lane;
+      cplx s = make_double2(0.0, 0.0);
+      if (c < k)
+        for (int i = j + warp; i < m; i += 8) {
+          cplx v = A[(size_t)i * k + j], a = A[(size_t)i * k + c];
+          s.x += v.x * a.x + v.y * a.y;
+          s.y += v.x * a.y - v.y * a.x;
+        }
+      cred[warp][lane] = s;
+      __syncthreads();
+      if (warp == 0) {
+        cplx t = make_double2(0.0, 0.0);
+        for (int w = 0; w < 8; ++w) { t.x += cred[w][lane].x; t.y += cred[w][lane].y; }
+        s_w[lane] = cmul(ctau, t);
+      }
+      __syncthreads();
+      if (c < k) {
+        const cplx w = s_w[lane];
+        for (int i = j + warp; i < m; i += 8) {
+          cplx v = A[(size_t)i * k + j];
+          cplx u = cmul(v, w);
+          cplx a = A[(size_t)i * k + c];
+          A[(size_t)i * k + c] = make_double2(a.x - u.x, a.y - u.y);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (size_t e = tid; e < (size_t)m * k; e += 256) {
+    int i = (int)(e / k), c = (int)(e % k);
+    Q[e] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  for (int j = k - 1; j >= 0; --j) {   // Q = H_j Q on columns c >= j
+    const cplx tau = P.tau[j];
+    if (tau.x == 0.0 && tau.y == 0.0) continue;
+    for (int c0 = j; c0 < k; c0 += 32) {
+      const int c = c0 + lane;
+      cplx s = make_double2(0.0, 0.0);
+      if (c < k)
+        for (int i = j + warp; i < m; i += 8) {
+          cplx v = A[(size_t)i * k + j], q = Q[(size_t)i * k + c];
+          s.x += v.x * q.x + v.y * q.y;
+          s.y += v.x * q.y - v.y * q.x;
+        }
+      cred[warp][lane] = s;
+      __syncthreads();
+      if (warp == 0) {
+        cplx t = make_double2(0.0, 0.0);
+        for (int w = 0; w < 8; ++w) { t.x += cred[w][lane].x; t.y += cred[w][lane].y; }
+        s_w[lane] = cmul(tau, t);
+      }
+      __syncthreads();
+      if (c < k) {
+        const cplx w = s_w[lane];
+        for (int i = j + warp; i < m; i += 8) {
+          cplx v = A[(size_t)i * k + j];
+          cplx u = cmul(v, w);
+          cplx q = Q[(size_t)i * k + c];
+          Q[(size_t)i * k + c] = make_double2(q.x - u.x, q.y - u.y);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 }  // namespace
+
+void launch_geqr_q(GeqrProblem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  const GeqrProblem* d = static_cast<const GeqrProblem*>(st.put(h, sizeof(GeqrProblem) * n));
+  double fl = 0.0;
+  for (int i = 0; i < n; ++i) fl += 16.0 * (double)h[i].m * h[i].k * h[i].k;
+  prof_begin(s);
+  geqr_q_grouped<<<n, 256, 0, s>>>(d);
+  prof_end(s, "geqr", fl, 0.0);
+  count_launch();
+}
 
 void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   const PotrfProblem* d = static_cast<const PotrfProblem*>(st.put(h, sizeof(PotrfProblem) * n));
+  double fl = 0.0;
+  for (int i = 0; i < n; ++i) fl += 8.0 * (double)h[i].n * h[i].n * h[i].n / 6.0;
+  prof_begin(s);
   potrf_grouped<<<n, 256, 0, s>>>(d);
+  prof_end(s, "potrf", fl, 0.0);
   count_launch();
 }
 
 void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   const TrtriProblem* d = static_cast<const TrtriProblem*>(st.put(h, sizeof(TrtriProblem) * n));
+  double fl = 0.0;
+  for (int i = 0; i < n; ++i) fl += 8.0 * (double)h[i].n * h[i].n * h[i].n / 6.0;
+  prof_begin(s);
   trtri_grouped<<<n, 256, 0, s>>>(d);
+  prof_end(s, "trtri", fl, 0.0);
   count_launch();
 }
 

@@ -14,6 +14,7 @@
 //   Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br.
 // Operands are staged in shared memory by a 3-stage cp.async (16 B per complex) pipeline.
 #include "kernels.h"
+#include "prof.h"
 #include <cstdio>
 #include <vector>
 #include <algorithm>
@@ -210,7 +211,14 @@ void launch_variant(GemmProblem* h, int n, Stager& st, cudaStream_t s) {
                          Smem<TA, TB>::BYTES);
     attr_done = true;
   }
+  double flops = 0.0, bytes = 0.0;
+  for (int i = 0; i < n; ++i) {
+    flops += 8.0 * (double)h[i].M * h[i].N * h[i].K;
+    bytes += 16.0 * ((double)h[i].M * h[i].K + (double)h[i].K * h[i].N + (double)h[i].M * h[i].N);
+  }
+  prof_begin(s);
   zgemm_grouped<TA, TB><<<tiles, THREADS, Smem<TA, TB>::BYTES, s>>>(d, n);
+  prof_end(s, "zgemm", flops, bytes);
   count_launch();
 }
 

@@ -16,6 +16,7 @@
 //  5. Truncation decision k = min(max_bond, #{lam > tol^2 lam_1}, #{lam > floor lam_1}) >= 1
 //     and discarded weight w = trace(A) - sum_{t<k} lam_t.
 #include "kernels.h"
+#include "prof.h"
 #include <cfloat>
 #include <cmath>
 
@@ -412,7 +413,15 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
     attr = true;
   }
   const HeevProblem* d = static_cast<const HeevProblem*>(st.put(h, sizeof(HeevProblem) * n));
+  double fl = 0.0, by = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double nn = h[i].n;
+    fl += 8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * h[i].kmax);
+    by += 16.0 * nn * nn;
+  }
+  prof_begin(s);
   heev_grouped<<<n, HEEV_THREADS, smem, s>>>(d);
+  prof_end(s, "heev", fl, by);
   count_launch();
 }
 

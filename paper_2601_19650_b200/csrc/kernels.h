@@ -112,6 +112,9 @@ void launch_scale_rows(ScaleRowsProblem* h, int n, Stager& st, cudaStream_t s);
 struct SumsqProblem { const cplx* x; long long len; double* out; };
 void launch_sumsq(SumsqProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_fill(cplx* p, long long n, cplx v, cudaStream_t s);
+// Householder QR of a tall m x k matrix A (ld k, destroyed) -> thin Q (m x k, ld k).
+struct GeqrProblem { cplx* A; cplx* Q; cplx* tau; int m; int k; };
+void launch_geqr_q(GeqrProblem* h, int n, Stager& st, cudaStream_t s);
 // P[i*ld + j] = (i == j) for i < m, j < ncols, grouped
 struct EyeProblem { cplx* p; int m; int ncols; long long start; };
 void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s);

@@ -3,6 +3,7 @@
 // scaling that forms the Gram-route factor L = Lambda^{1/2} V^H ("compressed ... via
 // singular value decomposition", reading A1/A2), Frobenius sums of squares for ||phi||.
 #include "kernels.h"
+#include "prof.h"
 #include <atomic>
 #include <algorithm>
 
@@ -101,7 +102,9 @@ void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s) {
   for (int i = 0; i < n; ++i) { h[i].start = total; total += h[i].total; }
   if (total == 0) return;
   const PermProblem* d = static_cast<const PermProblem*>(st.put(h, sizeof(PermProblem) * n));
+  prof_begin(s);
   permute_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  prof_end(s, "permute", 0.0, 32.0 * (double)total);
   count_launch();
 }
 
@@ -110,14 +113,18 @@ void launch_scale_rows(ScaleRowsProblem* h, int n, Stager& st, cudaStream_t s) {
   for (int i = 0; i < n; ++i) { h[i].start = total; total += (long long)h[i].kmax * h[i].n; }
   if (total == 0) return;
   const ScaleRowsProblem* d = static_cast<const ScaleRowsProblem*>(st.put(h, sizeof(ScaleRowsProblem) * n));
+  prof_begin(s);
   scale_rows_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  prof_end(s, "scale_rows", 0.0, 32.0 * (double)total);
   count_launch();
 }
 
 void launch_sumsq(SumsqProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   const SumsqProblem* d = static_cast<const SumsqProblem*>(st.put(h, sizeof(SumsqProblem) * n));
+  prof_begin(s);
   sumsq_kernel<<<n, 256, 0, s>>>(d);
+  prof_end(s, "misc", 0.0, 0.0);
   count_launch();
 }
 
@@ -126,13 +133,17 @@ void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s) {
   for (int i = 0; i < n; ++i) { h[i].start = total; total += (long long)h[i].m * h[i].ncols; }
   if (total == 0) return;
   const EyeProblem* d = static_cast<const EyeProblem*>(st.put(h, sizeof(EyeProblem) * n));
+  prof_begin(s);
   eye_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  prof_end(s, "misc", 0.0, 16.0 * (double)total);
   count_launch();
 }
 
 void launch_fill(cplx* p, long long n, cplx v, cudaStream_t s) {
   if (n <= 0) return;
+  prof_begin(s);
   fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
+  prof_end(s, "misc", 0.0, 16.0 * (double)n);
   count_launch();
 }
 

@@ -1,0 +1,115 @@
+#include "prof.h"
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace tcbc {
+
+namespace {
+
+struct Pending {
+  cudaEvent_t a, b;
+  std::string family;
+  double flops, bytes;
+};
+
+struct Acc {
+  double ms = 0.0, flops = 0.0, bytes = 0.0;
+  long long launches = 0;
+};
+
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<Pending> pending;
+  std::map<std::string, Acc> acc;
+  cudaEvent_t open = nullptr;
+
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void harvest() {
+    for (auto& p : pending) {
+      float ms = 0.f;
+      cudaEventSynchronize(p.b);
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      Acc& a = acc[p.family];
+      a.ms += ms;
+      a.flops += p.flops;
+      a.bytes += p.bytes;
+      a.launches += 1;
+      Acc& t = acc["all"];
+      t.ms += ms;
+      t.flops += p.flops;
+      t.bytes += p.bytes;
+      t.launches += 1;
+      pool.push_back(p.a);
+      pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+};
+
+Profiler& P() {
+  static Profiler p;
+  return p;
+}
+
+}  // namespace
+
+void prof_begin(cudaStream_t s) {
+  Profiler& p = P();
+  if (!p.on) return;
+  std::lock_guard<std::mutex> g(p.mu);
+  p.open = p.get();
+  cudaEventRecord(p.open, s);
+}
+
+void prof_end(cudaStream_t s, const char* family, double flops, double bytes) {
+  Profiler& p = P();
+  if (!p.on) return;
+  std::lock_guard<std::mutex> g(p.mu);
+  if (!p.open) return;
+  cudaEvent_t b = p.get();
+  cudaEventRecord(b, s);
+  p.pending.push_back(Pending{p.open, b, family, flops, bytes});
+  p.open = nullptr;
+  if (p.pending.size() > 4096) p.harvest();
+}
+
+void prof_enable(bool on) {
+  Profiler& p = P();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.harvest();
+  p.acc.clear();
+  p.on = on;
+}
+
+bool prof_read(const char* family, double* ms, double* flops, double* bytes, long long* launches) {
+  Profiler& p = P();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.harvest();
+  auto it = p.acc.find(family);
+  if (it == p.acc.end()) {
+    *ms = *flops = *bytes = 0.0;
+    *launches = 0;
+    return false;
+  }
+  *ms = it->second.ms;
+  *flops = it->second.flops;
+  *bytes = it->second.bytes;
+  *launches = it->second.launches;
+  return true;
+}
+
+}  // namespace tcbc

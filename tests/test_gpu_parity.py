@@ -170,3 +170,30 @@ def test_zero_state(P, ctx):
     out, rep = P.cbc_apply(ctx, op, z, 6)
     assert out.bonds() == [1] * 6
     assert rep["norm"] == 0.0
+
+
+def test_config5_circuit_layers(P, ctx):
+    """Config 5 (A15): 63-qubit circuit, 10 layers, seeds batched layer-synchronously.
+    Untruncated: ||phi|| = 1 after every layer (P13) and parity with the oracle."""
+    seeds = [0, 1, 2]
+    insts = [W.make_config(5, seed=s) for s in seeds]
+    parent = insts[0].parent
+    cur = [P.ttn_create(ctx, P.TTN_STATE, parent, i.phys, i.state_bond, i.state) for i in insts]
+    ors = [TTN(parent, [t.copy() for t in i.state]) for i in insts]
+    fallbacks = 0
+    for layer in range(10):
+        ops_h, ops_o = [], []
+        for s in seeds:
+            o, ob, _ = W.circuit_layer_operator(parent, s, layer)
+            ops_h.append(P.ttn_create(ctx, P.TTN_OPERATOR, parent, [2] * 63, ob, o))
+            ops_o.append(TTN(parent, o, "operator"))
+        cur, reps = P.cbc_apply_batch(ctx, ops_h, cur, 256)
+        ors = [oracle_cbc(oo, ps, 256) for oo, ps in zip(ops_o, ors)]
+        for r in reps:
+            assert abs(r["norm"] - 1.0) <= 1e-12
+            fallbacks += r["rank_fallbacks"]
+    for h, po in zip(cur, ors):
+        g = to_oracle(P, h, parent)
+        d_cos, d_rel = distances(g, po)
+        assert d_cos <= 1e-10 and d_rel <= 1e-6, (d_cos, d_rel)
+        assert g.bonds() == po.bonds()
