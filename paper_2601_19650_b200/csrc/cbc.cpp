@@ -102,19 +102,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     const int64_t kmax = std::min<int64_t>(max_bond, nn);
     kmaxs[j] = kmax;
     cplx* G = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
-    GemmProblem g{};
-    if (m >= n) {   // G = X^H X
-      g.A = J.X; g.opA = OP_C; g.lda = n;
-      g.B = J.X; g.opB = OP_N; g.ldb = n;
-      g.M = (int)n; g.N = (int)n; g.K = (int)m;
-    } else {        // K = X X^H
-      g.A = J.X; g.opA = OP_N; g.lda = n;
-      g.B = J.X; g.opB = OP_C; g.ldb = n;
-      g.M = (int)m; g.N = (int)m; g.K = (int)n;
-    }
-    g.C = G; g.ldc = nn;
-    g.alpha = make_double2(1.0, 0.0);
-    g.beta = make_double2(0.0, 0.0);
+    GemmProblem g = (m >= n) ? mk_gemm(J.X, OP_C, n, J.X, OP_N, n, G, nn, n, n, m)     // G = X^H X
+                             : mk_gemm(J.X, OP_N, n, J.X, OP_C, n, G, nn, m, m, n);    // K = X X^H
     grams.push_back(g);
     flops_inst[J.inst] += 8.0 * (double)g.M * g.N * g.K;
     HeevProblem& h = hp[j];
@@ -140,14 +129,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       s.Vt = h.Vt; s.lam = h.lam; s.F = J.dst->p; s.kmax = (int)kmax; s.n = (int)n;
       sr.push_back(s);
     } else {   // F = conj(Vt) X  (U_k^H X)
-      GemmProblem f{};
-      f.A = h.Vt; f.opA = OP_R; f.lda = m;
-      f.B = J.X; f.opB = OP_N; f.ldb = n;
-      f.C = J.dst->p; f.ldc = n;
-      f.M = (int)kmax; f.N = (int)n; f.K = (int)m;
-      f.alpha = make_double2(1.0, 0.0);
-      f.beta = make_double2(0.0, 0.0);
-      fgemm.push_back(f);
+      fgemm.push_back(mk_gemm(h.Vt, OP_R, m, J.X, OP_N, n, J.dst->p, n, kmax, n, m));
       flops_inst[J.inst] += 8.0 * (double)kmax * n * m;
     }
     st.peak_entries = std::max(st.peak_entries, nn * nn);
@@ -196,11 +178,7 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
     cplx* Li2 = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * k * k));
     auto gp = [&](const cplx* A, int opA, long long lda, const cplx* B, int opB, long long ldb, cplx* C, int64_t M,
                   int64_t N, int64_t K) {
-      GemmProblem g{};
-      g.A = A; g.opA = opA; g.lda = lda; g.B = B; g.opB = opB; g.ldb = ldb; g.C = C; g.ldc = N;
-      g.M = (int)M; g.N = (int)N; g.K = (int)K;
-      g.alpha = make_double2(1.0, 0.0);
-      g.beta = make_double2(0.0, 0.0);
+      GemmProblem g = mk_gemm(A, opA, lda, B, opB, ldb, C, N, M, N, K);
       flops_inst[J.inst] += 8.0 * (double)M * N * K;
       return g;
     };
@@ -313,7 +291,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
     }
     st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
     // per-instance flop share of the contraction (uniform tasks per instance)
-    for (auto& J : jobs) flops_inst[J.inst] += cs.flops / (double)jobs.size();
+    for (size_t j = 0; j < jobs.size(); ++j) flops_inst[jobs[j].inst] += tasks[j].flops;
     st.flops += cs.flops;
     compress_batch(ctx, jobs, max_bond, tol, st, w_inst, flops_inst);
     ctx->scratch.reset();
@@ -347,7 +325,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       jobs[j].m = tot / jobs[j].n;
     }
     st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-    for (auto& J : jobs) flops_inst[J.inst] += cs.flops / (double)jobs.size();
+    for (size_t j = 0; j < jobs.size(); ++j) flops_inst[jobs[j].inst] += tasks[j].flops;
     st.flops += cs.flops;
     compress_batch(ctx, jobs, max_bond, tol, st, w_inst, flops_inst);
     ctx->scratch.reset();
@@ -385,7 +363,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
     ExecStats cs;
     contract_batch(ctx, tasks, cs);
     st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-    for (auto& w : who) flops_inst[w.first] += cs.flops / (double)who.size();
+    for (size_t j = 0; j < who.size(); ++j) flops_inst[who[j].first] += tasks[j].flops;
     st.flops += cs.flops;
     std::vector<GemmProblem> sg, rg;
     std::vector<QRJob> qj;
@@ -400,14 +378,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       for (auto d : tasks[j].out_dims) tot *= d;
       const int64_t ms = tot / nz, kd = fd.k, r = rb[b][i];
       cplx* S = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * kd));
-      GemmProblem g{};   // S = Z Fd^T  (Eq. 12 via Z)
-      g.A = tasks[j].out; g.opA = OP_N; g.lda = nz;
-      g.B = fd.p; g.opB = OP_T; g.ldb = nz;
-      g.C = S; g.ldc = kd;
-      g.M = (int)ms; g.N = (int)kd; g.K = (int)nz;
-      g.alpha = make_double2(1.0, 0.0);
-      g.beta = make_double2(0.0, 0.0);
-      sg.push_back(g);
+      sg.push_back(mk_gemm(tasks[j].out, OP_N, nz, fd.p, OP_T, nz, S, kd, ms, kd, nz));   // S = Z Fd^T (Eq. 12 via Z)
       flops_inst[b] += 8.0 * (double)ms * kd * nz;
       cplx* Q = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * r));
       qj.push_back(QRJob{S, ms, kd, Q, b});
@@ -423,14 +394,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       Fac& Ri = R[(size_t)b * n + i];
       Ri.p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * r * nz));
       Ri.k = r; Ri.a = fd.a; Ri.b = fd.b;
-      GemmProblem h{};
-      h.A = Q; h.opA = OP_C; h.lda = r;
-      h.B = tasks[j].out; h.opB = OP_N; h.ldb = nz;
-      h.C = Ri.p; h.ldc = nz;
-      h.M = (int)r; h.N = (int)nz; h.K = (int)ms;
-      h.alpha = make_double2(1.0, 0.0);
-      h.beta = make_double2(0.0, 0.0);
-      rg.push_back(h);
+      rg.push_back(mk_gemm(Q, OP_C, r, tasks[j].out, OP_N, nz, Ri.p, nz, r, nz, ms));
       flops_inst[b] += 8.0 * (double)r * nz * ms;
     }
     gemm_batch(ctx, sg, st);

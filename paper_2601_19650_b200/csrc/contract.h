@@ -25,6 +25,7 @@ struct Task {
   std::vector<int> out_labels;
   cplx* out = nullptr;                 // destination; allocated from ctx->scratch when null
   std::vector<int64_t> out_dims;       // filled by contract_batch
+  double flops = 0.0;                  // filled by contract_batch (8 * complex MACs)
 };
 
 struct ExecStats {
@@ -36,5 +37,9 @@ void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st);
 
 // Convenience: grouped GEMM with host bookkeeping of flops.
 void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st);
+
+// Plain matrix product problem from BLAS-style op flags (OP_N/T/R/C) and leading dimensions.
+GemmProblem mk_gemm(const cplx* A, int opA, long long lda, const cplx* B, int opB, long long ldb, cplx* C,
+                    long long ldc, int64_t M, int64_t N, int64_t K);
 
 }  // namespace tcbc

@@ -1,36 +1,40 @@
-// Grouped complex-FP64 GEMM on the B200 FP64 tensor path (DMMA).
+// Grouped complex-FP64 tensor-contraction GEMM on the B200 FP64 tensor path (DMMA).
 //
 // Every contraction of the CBC hot path (Eqs. 10-12 and 14; the Grams
 // G = X^H X of B:5 (a); S = Z L^T; R = Q^H Z; factors U^H X) is lowered to
-//   C = alpha * op(A) op(B) + beta * C
-// over many independent problems of different shapes in one launch.
+//   C[m, n] = alpha * sum_k opA(A)[m, k] opB(B)[k, n] + beta * C[m, n]
+// where m, n, k are MULTI-indices (up to 6 legs each) addressed through arbitrary strides:
+// the leg permutations of the tensor network are fused into the operand loads and the
+// output store, so no transpose kernel ever runs between contraction steps.
 //
 // sm_100a has no tcgen05 kind::f64: FP64 tensor-core math is the warp-level
-// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Measured peak on this B200 pool: 37.1 TF/s
-// (profiles/fp64_peaks_r01.json).  One DMMA = 256 FMAs, so the SM issues one DMMA per
-// ~4 clocks: the kernel needs register blocking (32x32 complex warp tiles = 64 DMMA per
-// 8 LDS.128) rather than shared-memory bandwidth.
-// Complex product by the 4M rule on separate re/im accumulators:
-//   Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br.
-// Operands are staged in shared memory by a 3-stage cp.async (16 B per complex) pipeline.
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Measured peak on this pool: 37.1 TF/s
+// (profiles/fp64_peaks_r01.json).  One DMMA = 256 FMAs, so an SM retires one DMMA per
+// ~4 clocks: the kernel needs register blocking (warp tiles of 4x4 or 4x2 / 2x8 DMMA tiles)
+// more than shared-memory bandwidth.  Complex product by the 4M rule on separate re/im
+// accumulators:  Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br.
+// Operands are staged in shared memory by a 3-stage cp.async (16 B per complex) pipeline;
+// shared-memory layouts are chosen per problem (k-contiguous or m/n-contiguous legs) so the
+// global loads coalesce whenever one leg of the operand has unit stride.
 #include "kernels.h"
 #include "prof.h"
+#include <algorithm>
 #include <cstdio>
 #include <vector>
-#include <algorithm>
 
 namespace tcbc {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 8, STAGES = 3, THREADS = 128;
+constexpr int BK = 8, STAGES = 3, THREADS = 128;
 constexpr int PADK = BK + 4;   // m-major / n-major rows: 12 complex = 192 B (conflict-free frags)
 
-template <bool TA, bool TB>
-struct Smem {
-  static constexpr int A_ELEMS = TA ? BK * BM : BM * PADK;
-  static constexpr int B_ELEMS = TB ? BN * PADK : BK * BN;
-  static constexpr int BYTES = STAGES * (A_ELEMS + B_ELEMS) * 16;
+template <int BM, int BN, bool AKM, bool BNM>
+struct Cfg {
+  static constexpr int A_ELEMS = AKM ? BK * BM : BM * PADK;
+  static constexpr int B_ELEMS = BNM ? BN * PADK : BK * BN;
+  static constexpr int TAB = (2 * BM + 2 * BN) * 8;
+  static constexpr int BYTES = STAGES * (A_ELEMS + B_ELEMS) * 16 + TAB + 1024;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -48,6 +52,18 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// offset of multi-index x in a group of n legs (row-major: last leg fastest)
+__device__ __forceinline__ long long goff(int x, int n, const int* d, const long long* s) {
+  long long off = 0;
+#pragma unroll 1
+  for (int i = n - 1; i >= 0; --i) {
+    int q = x / d[i];
+    off += (long long)(x - q * d[i]) * s[i];
+    x = q;
+  }
+  return off;
+}
+
 __device__ __forceinline__ int find_problem(const GemmProblem* p, int n, int tile) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -57,61 +73,100 @@ __device__ __forceinline__ int find_problem(const GemmProblem* p, int n, int til
   return lo;
 }
 
-template <bool TA, bool TB>
+template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
 __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob) {
+  using C_ = Cfg<BM, BN, AKM, BNM>;
+  constexpr int WTM = BM / WGM, WTN = BN / WGN;     // warp tile
+  constexpr int TM = WTM / 8, TN = WTN / 8;         // DMMA tiles per warp
+  static_assert(WGM * WGN == THREADS / 32, "warp grid");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
-  cplx* Bs = As + STAGES * Smem<TA, TB>::A_ELEMS;
+  cplx* Bs = As + STAGES * C_::A_ELEMS;
+  long long* rowA = reinterpret_cast<long long*>(Bs + STAGES * C_::B_ELEMS);
+  long long* colB = rowA + BM;
+  long long* rowC = colB + BN;
+  long long* colC = rowC + BM;
+  GemmProblem* sP = reinterpret_cast<GemmProblem*>(colC + BN);
 
-  const int pi = find_problem(probs, nprob, blockIdx.x);
-  const GemmProblem P = probs[pi];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) *sP = probs[find_problem(probs, nprob, blockIdx.x)];
+  __syncthreads();
+  const GemmProblem& P = *sP;
   const int t = blockIdx.x - P.tile_start;
   const int m0 = (t / P.tiles_n) * BM, n0 = (t % P.tiles_n) * BN;
   const int M = P.M, N = P.N, K = P.K;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  const bool conjA = (P.opA & 2) != 0, conjB = (P.opB & 2) != 0;
+  for (int i = tid; i < BM; i += THREADS) {
+    const int m = m0 + i;
+    rowA[i] = m < M ? goff(m, P.nm, P.md, P.am) : -1;
+    rowC[i] = m < M ? goff(m, P.nm, P.md, P.cm) : -1;
+  }
+  for (int i = tid; i < BN; i += THREADS) {
+    const int n = n0 + i;
+    colB[i] = n < N ? goff(n, P.nn, P.nd, P.bn) : -1;
+    colC[i] = n < N ? goff(n, P.nn, P.nd, P.cn) : -1;
+  }
+  __syncthreads();
+  const cplx* __restrict__ Ag = P.A;
+  const cplx* __restrict__ Bg = P.B;
+  const int wm = (warp / WGN) * WTM, wn = (warp % WGN) * WTN;
+  const bool conjA = P.conjA != 0, conjB = P.conjB != 0;
 
   auto load_stage = [&](int stage, int k0) {
-    cplx* as = As + stage * Smem<TA, TB>::A_ELEMS;
-    cplx* bs = Bs + stage * Smem<TA, TB>::B_ELEMS;
+    cplx* as = As + stage * C_::A_ELEMS;
+    cplx* bs = Bs + stage * C_::B_ELEMS;
+    if (!AKM) {   // As[m][k]: k fixed per thread
+      const int k = tid % BK;
+      const bool kv = k0 + k < K;
+      const long long ko = kv ? goff(k0 + k, P.nk, P.kd, P.ak) : 0;
 #pragma unroll
-    for (int r = 0; r < (BM * BK) / THREADS; ++r) {
-      int idx = tid + r * THREADS;
-      if (!TA) {
-        int m = idx / BK, k = idx % BK;
-        bool v = (m0 + m < M) && (k0 + k < K);
-        const cplx* src = v ? P.A + (long long)(m0 + m) * P.lda + (k0 + k) : P.A;
-        cp_async16(as + m * PADK + k, src, v);
-      } else {
-        int k = idx / BM, m = idx % BM;
-        bool v = (m0 + m < M) && (k0 + k < K);
-        const cplx* src = v ? P.A + (long long)(k0 + k) * P.lda + (m0 + m) : P.A;
-        cp_async16(as + k * BM + m, src, v);
+      for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+        const int m = tid / BK + r * (THREADS / BK);
+        const long long ro = rowA[m];
+        const bool v = kv && ro >= 0;
+        cp_async16(as + m * PADK + k, v ? Ag + ro + ko : Ag, v);
+      }
+    } else {      // As[k][m]
+#pragma unroll
+      for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+        const int idx = tid + r * THREADS;
+        const int k = idx / BM, m = idx % BM;
+        const bool kv = k0 + k < K;
+        const long long ro = rowA[m];
+        const bool v = kv && ro >= 0;
+        const long long ko = v ? goff(k0 + k, P.nk, P.kd, P.ak) : 0;
+        cp_async16(as + k * BM + m, v ? Ag + ro + ko : Ag, v);
       }
     }
+    if (BNM) {    // Bs[n][k]: k fixed per thread
+      const int k = tid % BK;
+      const bool kv = k0 + k < K;
+      const long long ko = kv ? goff(k0 + k, P.nk, P.kd, P.bk) : 0;
 #pragma unroll
-    for (int r = 0; r < (BN * BK) / THREADS; ++r) {
-      int idx = tid + r * THREADS;
-      if (!TB) {
-        int k = idx / BN, n = idx % BN;
-        bool v = (n0 + n < N) && (k0 + k < K);
-        const cplx* src = v ? P.B + (long long)(k0 + k) * P.ldb + (n0 + n) : P.B;
-        cp_async16(bs + k * BN + n, src, v);
-      } else {
-        int n = idx / BK, k = idx % BK;
-        bool v = (n0 + n < N) && (k0 + k < K);
-        const cplx* src = v ? P.B + (long long)(n0 + n) * P.ldb + (k0 + k) : P.B;
-        cp_async16(bs + n * PADK + k, src, v);
+      for (int r = 0; r < (BN * BK) / THREADS; ++r) {
+        const int n = tid / BK + r * (THREADS / BK);
+        const long long co = colB[n];
+        const bool v = kv && co >= 0;
+        cp_async16(bs + n * PADK + k, v ? Bg + co + ko : Bg, v);
+      }
+    } else {      // Bs[k][n]
+#pragma unroll
+      for (int r = 0; r < (BN * BK) / THREADS; ++r) {
+        const int idx = tid + r * THREADS;
+        const int k = idx / BN, n = idx % BN;
+        const bool kv = k0 + k < K;
+        const long long co = colB[n];
+        const bool v = kv && co >= 0;
+        const long long ko = v ? goff(k0 + k, P.nk, P.kd, P.bk) : 0;
+        cp_async16(bs + k * BN + n, v ? Bg + co + ko : Bg, v);
       }
     }
   };
 
-  double acc_re[4][4][2], acc_im[4][4][2];
+  double acc_re[TM][TN][2], acc_im[TM][TN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < TN; ++j) {
       acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
       acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
     }
@@ -127,35 +182,35 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {  // prefetch stage kt + STAGES - 1 (its buffer was consumed at iteration kt - 1)
-      int kn = kt + STAGES - 1;
+    {
+      const int kn = kt + STAGES - 1;
       if (kn < ktiles) load_stage(kn % STAGES, kn * BK);
       cp_async_commit();
     }
-    const cplx* as = As + (kt % STAGES) * Smem<TA, TB>::A_ELEMS;
-    const cplx* bs = Bs + (kt % STAGES) * Smem<TA, TB>::B_ELEMS;
+    const cplx* as = As + (kt % STAGES) * C_::A_ELEMS;
+    const cplx* bs = Bs + (kt % STAGES) * C_::B_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double ar[4], ai[4], nai[4], br[4], bi[4];
+      double ar[TM], ai[TM], nai[TM], br[TN], bi[TN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int m = wm + i * 8 + fr, k = kk + fc;
-        cplx a = TA ? as[k * BM + m] : as[m * PADK + k];
+      for (int i = 0; i < TM; ++i) {
+        const int m = wm + i * 8 + fr, k = kk + fc;
+        const cplx a = AKM ? as[k * BM + m] : as[m * PADK + k];
         ar[i] = a.x;
         ai[i] = conjA ? -a.y : a.y;
         nai[i] = -ai[i];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int n = wn + j * 8 + fr, k = kk + fc;
-        cplx b = TB ? bs[n * PADK + k] : bs[k * BN + n];
+      for (int j = 0; j < TN; ++j) {
+        const int n = wn + j * 8 + fr, k = kk + fc;
+        const cplx b = BNM ? bs[n * PADK + k] : bs[k * BN + n];
         br[j] = b.x;
         bi[j] = conjB ? -b.y : b.y;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < TN; ++j) {
           dmma(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
           dmma(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
           dmma(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
@@ -165,26 +220,27 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
   }
   cp_async_wait<0>();
 
-  // epilogue: C = alpha * acc + beta * C
+  // epilogue: C = alpha * acc + beta * C (strided store: the output permutation is fused here)
   const cplx al = P.alpha, be = P.beta;
   const bool use_beta = (be.x != 0.0 || be.y != 0.0);
+  cplx* __restrict__ Cg = P.C;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int m = m0 + wm + i * 8 + fr;
-    if (m >= M) continue;
+  for (int i = 0; i < TM; ++i) {
+    const long long ro = rowC[wm + i * 8 + fr];
+    if (ro < 0) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < TN; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int n = n0 + wn + j * 8 + fc * 2 + h;
-        if (n >= N) continue;
-        double re = acc_re[i][j][h], im = acc_im[i][j][h];
+        const long long co = colC[wn + j * 8 + fc * 2 + h];
+        if (co < 0) continue;
+        const double re = acc_re[i][j][h], im = acc_im[i][j][h];
         cplx out;
         out.x = al.x * re - al.y * im;
         out.y = al.x * im + al.y * re;
-        cplx* cp = P.C + (long long)m * P.ldc + n;
+        cplx* cp = Cg + ro + co;
         if (use_beta) {
-          cplx c = *cp;
+          const cplx c = *cp;
           out.x += be.x * c.x - be.y * c.y;
           out.y += be.x * c.y + be.y * c.x;
         }
@@ -194,47 +250,75 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
   }
 }
 
-template <bool TA, bool TB>
-void launch_variant(GemmProblem* h, int n, Stager& st, cudaStream_t s) {
+template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
+void launch_variant(std::vector<GemmProblem>& h, Stager& st, cudaStream_t s) {
+  if (h.empty()) return;
   int tiles = 0;
-  for (int i = 0; i < n; ++i) {
-    int tm = (h[i].M + BM - 1) / BM, tn = (h[i].N + BN - 1) / BN;
-    h[i].tile_start = tiles;
-    h[i].tiles_n = std::max(tn, 1);
+  double flops = 0.0, bytes = 0.0;
+  for (auto& p : h) {
+    const int tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
+    p.tile_start = tiles;
+    p.tiles_n = std::max(tn, 1);
     tiles += tm * tn;
+    flops += 8.0 * (double)p.M * p.N * p.K;
+    bytes += 16.0 * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N);
   }
   if (tiles == 0) return;
-  const GemmProblem* d = static_cast<const GemmProblem*>(st.put(h, sizeof(GemmProblem) * n));
+  const GemmProblem* d = static_cast<const GemmProblem*>(st.put(h.data(), sizeof(GemmProblem) * h.size()));
+  using C_ = Cfg<BM, BN, AKM, BNM>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(zgemm_grouped<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Smem<TA, TB>::BYTES);
+    cudaFuncSetAttribute(zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C_::BYTES);
     attr_done = true;
   }
-  double flops = 0.0, bytes = 0.0;
-  for (int i = 0; i < n; ++i) {
-    flops += 8.0 * (double)h[i].M * h[i].N * h[i].K;
-    bytes += 16.0 * ((double)h[i].M * h[i].K + (double)h[i].K * h[i].N + (double)h[i].M * h[i].N);
-  }
   prof_begin(s);
-  zgemm_grouped<TA, TB><<<tiles, THREADS, Smem<TA, TB>::BYTES, s>>>(d, n);
+  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM><<<tiles, THREADS, C_::BYTES, s>>>(d, (int)h.size());
   prof_end(s, "zgemm", flops, bytes);
   count_launch();
 }
 
+template <int BM, int BN, int WGM, int WGN>
+void launch_shape(std::vector<GemmProblem>* g4, Stager& st, cudaStream_t s) {
+  launch_variant<BM, BN, WGM, WGN, false, false>(g4[0], st, s);
+  launch_variant<BM, BN, WGM, WGN, false, true>(g4[1], st, s);
+  launch_variant<BM, BN, WGM, WGN, true, false>(g4[2], st, s);
+  launch_variant<BM, BN, WGM, WGN, true, true>(g4[3], st, s);
+}
+
 }  // namespace
 
+void gemm_from_ops(GemmProblem& g, int opA, long long lda, int opB, long long ldb, long long ldc) {
+  g.nm = g.nn = g.nk = 1;
+  g.md[0] = g.M;
+  g.nd[0] = g.N;
+  g.kd[0] = g.K;
+  if (opA & 1) { g.am[0] = 1; g.ak[0] = lda; } else { g.am[0] = lda; g.ak[0] = 1; }
+  if (opB & 1) { g.bn[0] = ldb; g.bk[0] = 1; } else { g.bk[0] = ldb; g.bn[0] = 1; }
+  g.cm[0] = ldc;
+  g.cn[0] = 1;
+  g.conjA = (opA & 2) ? 1 : 0;
+  g.conjB = (opB & 2) ? 1 : 0;
+}
+
 void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s) {
-  // split by storage layout (transpose bits); conjugation is a runtime flag
-  std::vector<GemmProblem> g[4];
+  // group by tile shape (skinny N / skinny M / square) and shared-memory layouts
+  std::vector<GemmProblem> sq[4], tall[4], wide[4];
   for (int i = 0; i < n; ++i) {
-    if (h[i].M <= 0 || h[i].N <= 0) continue;
-    g[(h[i].opA & 1) * 2 + (h[i].opB & 1)].push_back(h[i]);
+    GemmProblem p = h[i];
+    if (p.M <= 0 || p.N <= 0) continue;
+    // A: k-major smem when the innermost m leg is unit-stride and the innermost k leg is not
+    const bool akm = (p.ak[p.nk - 1] != 1) && (p.am[p.nm - 1] == 1);
+    // B: n-major smem when the innermost k leg is unit-stride and the innermost n leg is not
+    const bool bnm = (p.bn[p.nn - 1] != 1) && (p.bk[p.nk - 1] == 1);
+    const int v = (akm ? 2 : 0) + (bnm ? 1 : 0);
+    if (p.N <= 16 && p.M > 16) tall[v].push_back(p);
+    else if (p.M <= 16 && p.N > 16) wide[v].push_back(p);
+    else sq[v].push_back(p);
   }
-  if (!g[0].empty()) launch_variant<false, false>(g[0].data(), (int)g[0].size(), st, s);
-  if (!g[1].empty()) launch_variant<false, true>(g[1].data(), (int)g[1].size(), st, s);
-  if (!g[2].empty()) launch_variant<true, false>(g[2].data(), (int)g[2].size(), st, s);
-  if (!g[3].empty()) launch_variant<true, true>(g[3].data(), (int)g[3].size(), st, s);
+  launch_shape<64, 64, 2, 2>(sq, st, s);
+  launch_shape<128, 16, 4, 1>(tall, st, s);
+  launch_shape<16, 128, 1, 4>(wide, st, s);
 }
 
 }  // namespace tcbc

@@ -12,21 +12,28 @@ typedef double2 cplx;   // (x = re, y = im), 16-byte aligned
 // op bits: bit0 = transpose, bit1 = conjugate
 enum { OP_N = 0, OP_T = 1, OP_R = 2 /*conj, no transpose*/, OP_C = 3 /*conj transpose*/ };
 
-// C[M,N] = alpha * op(A)[M,K] * op(B)[K,N] + beta * C.  Row-major storage:
-//   op(A) untransposed: A[m*lda + k];  transposed: A[k*lda + m]
-//   op(B) untransposed: B[k*ldb + n];  transposed: B[n*ldb + k]
+// Strided tensor-contraction GEMM:
+//   C[m, n] = alpha * sum_k opA(A)[m, k] * opB(B)[k, n] + beta * C[m, n]
+// m, n, k are multi-indices over nm / nn / nk legs (extents md / nd / kd, row-major: the last
+// leg fastest); element offsets are sum_leg index * stride with per-operand strides
+// (am, ak for A; bk, bn for B; cm, cn for C).  conjA / conjB conjugate the operand.
+constexpr int GEMM_MAXD = 6;
 struct GemmProblem {
   const cplx* A;
   const cplx* B;
   cplx* C;
-  long long lda, ldb, ldc;
   int M, N, K;
-  int opA, opB;
+  int conjA, conjB;
+  int nm, nn, nk;
+  int md[GEMM_MAXD], nd[GEMM_MAXD], kd[GEMM_MAXD];
+  long long am[GEMM_MAXD], ak[GEMM_MAXD], bk[GEMM_MAXD], bn[GEMM_MAXD], cm[GEMM_MAXD], cn[GEMM_MAXD];
   int tile_start;      // filled by the launcher
   int tiles_n;         // filled by the launcher
-  int pad_;
   cplx alpha, beta;
 };
+// Fill the leg descriptors of a plain matrix product from BLAS-style op flags
+// (bit0 transpose: A stored K x M / B stored N x K; bit1 conjugate) and leading dimensions.
+void gemm_from_ops(GemmProblem& g, int opA, long long lda, int opB, long long ldb, long long ldc);
 
 // dst[i] = (conj?) src[offset(i)], dst contiguous with dims[0..rank) (row-major);
 // sstride[r] is the source stride of destination axis r.

@@ -6,6 +6,8 @@
 #include "prof.h"
 #include <atomic>
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace tcbc {
 
@@ -102,6 +104,12 @@ void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s) {
   for (int i = 0; i < n; ++i) { h[i].start = total; total += h[i].total; }
   if (total == 0) return;
   const PermProblem* d = static_cast<const PermProblem*>(st.put(h, sizeof(PermProblem) * n));
+  static const bool dbg = getenv("TTN_DEBUG_GEMM") != nullptr;
+  if (dbg) {
+    fprintf(stderr, "[perm] %d problems, %lld elems; first rank %d dims", n, total, h[0].rank);
+    for (int r = 0; r < h[0].rank; ++r) fprintf(stderr, " %lld/%lld", h[0].dims[r], h[0].sstride[r]);
+    fprintf(stderr, "\n");
+  }
   prof_begin(s);
   permute_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
   prof_end(s, "permute", 0.0, 32.0 * (double)total);
