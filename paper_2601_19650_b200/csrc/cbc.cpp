@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 
 namespace tcbc {
@@ -135,6 +137,15 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     st.peak_entries = std::max(st.peak_entries, nn * nn);
   }
   gemm_batch(ctx, grams, st);
+  static const bool dump = getenv("TTN_DEBUG_HEEV") && std::string(getenv("TTN_DEBUG_HEEV")) == "3";
+  std::vector<std::vector<cplx>> gcopy;
+  if (dump) {   // debug: keep the Grams (heev destroys them) to dump the ones that fail
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& h : hp) {
+      gcopy.emplace_back((size_t)h.n * h.n);
+      cudaMemcpy(gcopy.back().data(), h.A, sizeof(cplx) * h.n * h.n, cudaMemcpyDeviceToHost);
+    }
+  }
   launch_heev(hp.data(), nj, *ctx->stager, ctx->stream);
   if (!sr.empty()) launch_scale_rows(sr.data(), (int)sr.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, fgemm, st);
@@ -145,6 +156,36 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   TTN_CUDA(cudaMemcpyAsync(hk, d_k, sizeof(int) * nj, cudaMemcpyDeviceToHost, ctx->stream));
   TTN_CUDA(cudaMemcpyAsync(hw, d_w, sizeof(double) * nj, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();
+  static const bool dbg = getenv("TTN_DEBUG_HEEV") != nullptr;
+  if (dbg) {   // debug: every eigenvector block and factor must be finite
+    for (int j = 0; j < nj; ++j) {
+      const HeevProblem& h = hp[j];
+      std::vector<cplx> vt((size_t)h.kmax * h.n), f((size_t)h.kmax * jobs[j].n);
+      std::vector<double> lam(h.kmax);
+      cudaMemcpy(vt.data(), h.Vt, sizeof(cplx) * vt.size(), cudaMemcpyDeviceToHost);
+      cudaMemcpy(f.data(), jobs[j].dst->p, sizeof(cplx) * f.size(), cudaMemcpyDeviceToHost);
+      cudaMemcpy(lam.data(), h.lam, sizeof(double) * lam.size(), cudaMemcpyDeviceToHost);
+      bool ok = true;
+      for (auto& v : vt) ok = ok && std::isfinite(v.x) && std::isfinite(v.y);
+      bool okf = true;
+      for (auto& v : f) okf = okf && std::isfinite(v.x) && std::isfinite(v.y);
+      std::vector<cplx> xx((size_t)jobs[j].m * jobs[j].n);
+      cudaMemcpy(xx.data(), jobs[j].X, sizeof(cplx) * xx.size(), cudaMemcpyDeviceToHost);
+      bool okx = true;
+      for (auto& v : xx) okx = okx && std::isfinite(v.x) && std::isfinite(v.y);
+      static const bool all = std::string(getenv("TTN_DEBUG_HEEV")) == "2";
+      if (dump && !ok) {
+        char fn[256];
+        snprintf(fn, sizeof(fn), "gpurun_out/bad_gram_%d_n%d_k%d.bin", j, h.n, h.kmax);
+        FILE* fp = fopen(fn, "wb");
+        if (fp) { fwrite(gcopy[j].data(), sizeof(cplx), gcopy[j].size(), fp); fclose(fp); }
+      }
+      if (!ok || !okf || !okx || all)
+        fprintf(stderr, "[heev] job %d F=%p m=%lld n=%lld nn=%d kmax=%d k=%d w=%g lam0=%g lamk=%g Vt_finite=%d F_finite=%d X_finite=%d\n", j,
+                (void*)jobs[j].dst->p, (long long)jobs[j].m, (long long)jobs[j].n, h.n, h.kmax, hk[j], hw[j], lam[0],
+                lam[h.kmax - 1], ok, okf, okx);
+    }
+  }
   for (int j = 0; j < nj; ++j) {
     if (hk[j] < 1 || hk[j] > kmaxs[j]) throw Error(TTN_ERR_NUMERIC, "eigensolver returned an invalid rank");
     if (!std::isfinite(hw[j])) throw Error(TTN_ERR_NUMERIC, "non-finite discarded weight (non-finite input?)");

@@ -60,12 +60,12 @@ struct HeevProblem {
   cplx* Vt;
   int* k_out;          // may be null
   double* w_out;       // may be null
-  double* work;        // real workspace, heev_work_doubles(n) entries
+  double* work;        // real workspace, heev_work_doubles(n, kmax) entries
   cplx* tau;           // n entries
   double tol2;         // tol^2
   double floor_rel;    // rank floor on lam / lam_1
   int max_bond;
-  int pad_;
+  int estart;          // filled by the launcher: prefix sum of kmax (eigenpair task index)
 };
 size_t heev_work_doubles(int n, int kmax);
 size_t heev_smem_bytes(int n, int kmax);

@@ -163,6 +163,27 @@ def test_errors(P, ctx):
         P.ttn_create(ctx, P.TTN_STATE, [-1, -1], [2, 2], [1, 1], [np.zeros((2, 1)), np.zeros((2, 1))])
 
 
+@pytest.mark.parametrize("d", [8, 64, 160, 200])
+def test_degenerate_spectrum_identity_gram(P, ctx, d):
+    """Edge case: leaves that are isometries give Gram = I (all eigenvalues equal, A21 tie);
+    untruncated the result is exact whatever basis the eigensolver picks."""
+    parent = [-1, 0, 0]
+    rng = np.random.default_rng(5)
+    eye = np.eye(d, dtype=np.complex128)
+    root = W.complex_gaussian(rng, (2, 1, d, d))
+    ops = W.identity_operator(parent, [2, d, d])
+    st = [root, eye, eye]
+    op_o = TTN(parent, ops, "operator")
+    psi = TTN(parent, st)
+    hs = P.ttn_create(ctx, P.TTN_STATE, parent, [2, d, d], [1, d, d], st)
+    ho = P.ttn_create(ctx, P.TTN_OPERATOR, parent, [2, d, d], [1, 1, 1], ops)
+    out, rep = P.cbc_apply(ctx, ho, hs, d)
+    phi_g = to_oracle(P, out, parent)
+    a, b = to_dense_state(phi_g), to_dense_state(psi)      # overlap distances floor at ~1e-8 (A18)
+    assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+    assert abs(rep["norm"] - norm(psi)) <= 1e-12 * norm(psi)
+
+
 def test_zero_state(P, ctx):
     inst = W.make_config(1, max_bond=6)
     op, _ = gpu_pair(P, ctx, inst)
