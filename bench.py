@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 5])
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -58,6 +58,10 @@ def workload_desc(cfg, batch):
     if cfg == 2:
         return {"workload": "BASELINE config 2: MPO.MPS chain N=32, d=2, chi=64, D=8, max_bond=64, single instance",
                 "batch_per_gpu": batch, "l2": "inputs (3.9 MB) fit in L2: L2 flushed between steps"}
+    if cfg == 4:
+        return {"workload": "BASELINE config 4 (reading A12): 67-node T3NS, root d=2 -> 2 junctions d=1 -> 4 chains x 16 "
+                            "nodes d=2, chi=128, D=16, max_bond=128, complex128 Gaussian, single instance",
+                "batch_per_gpu": batch, "l2": "inputs (34 MB) fit in L2: L2 flushed between steps"}
     if cfg == 5:
         return {"workload": f"BASELINE config 5: 63-qubit binary-tree circuit from |0..0>, 10 layers of Haar 2-qubit "
                             f"gates on seeded matchings, max_bond=256, {batch} seeds; a step = 10 layers x {batch} seeds",
@@ -169,7 +173,7 @@ def run_reference(args, rank, world):
         napp += n
     tot = sum(times)
     value = napp / tot
-    batch = args.batch or {3: 64, 2: 1, 5: 64, 1: 1}[cfg]
+    batch = args.batch or {3: 64, 2: 1, 4: 1, 5: 64, 1: 1}[cfg]
     line = {"metric": "CBC TTNO.TTNS applies/sec (FP64)", "value": value, "unit": "applies/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
@@ -189,7 +193,7 @@ def run_native(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     cfg = args.config
-    batch = args.batch or {3: 64, 2: 1, 5: 64, 1: 1}[cfg]
+    batch = args.batch or {3: 64, 2: 1, 4: 1, 5: 64, 1: 1}[cfg]
     seeds = [rank * batch + i for i in range(batch)]
     insts = make_instances(cfg, seeds)
     stream = torch.cuda.Stream(local_rank)
@@ -223,7 +227,7 @@ def run_native(args, rank, world, local_rank):
         ops = [P.ttn_create(ctx, P.TTN_OPERATOR, i.parent, i.phys, i.op_bond, i.op) for i in insts]
 
     flush = None
-    if cfg in (2, 5):
+    if cfg in (2, 4, 5):
         flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local_rank}")
 
     def step():
@@ -277,7 +281,7 @@ def run_native(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     launches = P.ttn_launch_count() - lc0
-    prof = {fam: P.ttn_profile_read(fam) for fam in ("all", "zgemm", "heev", "potrf", "trtri", "geqr", "permute",
+    prof = {fam: P.ttn_profile_read(fam) for fam in ("all", "zgemm", "heev", "heev_large", "potrf", "trtri", "geqr", "permute",
                                                      "scale_rows", "misc")}
     P.ttn_profile_enable(False)
     clk = clocks.stop(local_rank) if clocks else None

@@ -9,6 +9,7 @@
 //   assembly          T'_root = Z_root
 // Host synchronisation: once per compress level (data-dependent ranks) and once per final
 // level (Cholesky pivot flags).
+#include "chfsi.h"
 #include "contract.h"
 #include "runtime.h"
 
@@ -100,8 +101,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   for (int j = 0; j < nj; ++j) {
     CompressJob& J = jobs[j];
     const int64_t m = J.m, n = J.n, nn = std::min(m, n);
-    check_heev_size(nn);
     const int64_t kmax = std::min<int64_t>(max_bond, nn);
+    if (!chfsi_applicable((int)std::min<int64_t>(nn, INT32_MAX), (int)kmax)) check_heev_size(nn);
     kmaxs[j] = kmax;
     cplx* G = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
     GemmProblem g = (m >= n) ? mk_gemm(J.X, OP_C, n, J.X, OP_N, n, G, nn, n, n, m)     // G = X^H X
@@ -146,7 +147,16 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       cudaMemcpy(gcopy.back().data(), h.A, sizeof(cplx) * h.n * h.n, cudaMemcpyDeviceToHost);
     }
   }
-  launch_heev(hp.data(), nj, *ctx->stager, ctx->stream);
+  {   // small Grams: tridiagonal pipeline (heev.cu); large ones: Chebyshev subspace (chfsi.cu)
+    std::vector<HeevProblem> small;
+    std::vector<HeevProblem*> large;
+    for (auto& h : hp) {
+      if (chfsi_applicable(h.n, h.kmax)) large.push_back(&h);
+      else small.push_back(h);
+    }
+    if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream);
+    chfsi_heev(ctx, large, st);
+  }
   if (!sr.empty()) launch_scale_rows(sr.data(), (int)sr.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, fgemm, st);
   // read ranks and discarded weights

@@ -1,0 +1,407 @@
+// Top-k eigenpairs of LARGE compress Grams (n > kLargeN, e.g. BASELINE config 4's junction
+// Grams, n = 2048, k = 128) by Chebyshev-filtered subspace iteration with Rayleigh-Ritz.
+//
+// Why not the tridiagonal pipeline of heev.cu: a one-stage Householder tridiagonalisation is
+// BLAS-2 -- it streams the trailing matrix once per column, n^3/3 complex reads (46 GB for
+// n = 2048) through L2/HBM, seconds per matrix.  CBC only needs the top-k eigenspace of the
+// Gram (reading A1/A2: the same kept subspace as the truncated SVD), and here k << n, so
+// the work is re-expressed as dense complex GEMMs on the DMMA path (gemm.cu), where B200's
+// FP64 throughput lives:
+//   V <- orth(random n x p),  p = kmax + oversampling
+//   repeat:  Rayleigh-Ritz  W = G V, H = V^H W = Z Theta Z^H (heev.cu, p <= 512), V <- V Z,
+//            residuals r_t = ||W z_t - theta_t V z_t|| for the wanted t < kmax;
+//            stop when every wanted r_t <= kResTol * theta_1;
+//            otherwise filter V <- p_m(G) V D with the scaled three-term Chebyshev recurrence
+//            (Zhou & Saad) damping [0, theta_p] (the unwanted end of the spectrum of a PSD
+//            Gram), D = diag(1 / p_m(theta_j)) keeping the columns O(1), then CholeskyQR2.
+// Every Chebyshev degree is ONE grouped GEMM over all matrices of the level:
+//   Y_{j+1} = a_j (G - c I) Y_j - b_j Y_{j-1}   (in place over Y_{j-1}: C = alpha A B + beta C).
+// The result is written in heev.cu's HeevProblem contract (lam descending, Vt rows = eigenvectors,
+// k = min(max_bond, #{lam > tol^2 lam_1}, #{lam > floor lam_1}) >= 1, w = trace - sum_{t<k} lam_t),
+// so the factor formation downstream is shared.  Accuracy: the kept subspace is accurate to
+// ~ r / gap (Davis-Kahan); r <= 1e-12 lambda_1 is far inside the parity budget (1 - cos <= 1e-10).
+#include "chfsi.h"
+#include "prof.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+namespace tcbc {
+
+namespace {
+
+constexpr double kResTol = 1e-12;   // converged: ||G v - theta v|| <= kResTol * theta_1
+constexpr int kMaxIter = 12;
+
+__device__ __forceinline__ unsigned hash32(unsigned x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+  return x;
+}
+
+struct LargeDev {
+  const cplx* G;    // n x n (full Hermitian)
+  cplx* Gs;         // n x n shifted copy
+  cplx* V;          // n x p
+  double* dscale;   // p column scales
+  double shift;
+  int n, p;
+};
+
+__global__ void random_fill(LargeDev* P) {
+  const LargeDev& L = P[blockIdx.y];
+  const long long tot = (long long)L.n * L.p;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned h1 = hash32((unsigned)(i * 2 + 1) ^ 0x9e3779b9u), h2 = hash32((unsigned)(i * 2 + 2) ^ 0x7f4a7c15u);
+    L.V[i] = make_double2((h1 & 0xffffff) / 16777216.0 - 0.5, (h2 & 0xffffff) / 16777216.0 - 0.5);
+  }
+}
+
+__global__ void shift_copy(LargeDev* P) {
+  const LargeDev& L = P[blockIdx.y];
+  const long long tot = (long long)L.n * L.n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+    cplx v = L.G[i];
+    if (i / L.n == i % L.n) v.x -= L.shift;
+    L.Gs[i] = v;
+  }
+}
+
+__global__ void col_scale(LargeDev* P) {
+  const LargeDev& L = P[blockIdx.y];
+  const long long tot = (long long)L.n * L.p;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+    const double s = L.dscale[i % L.p];
+    L.V[i].x *= s;
+    L.V[i].y *= s;
+  }
+}
+
+struct ResDev {
+  const cplx* V;     // n x p Ritz vectors
+  const cplx* W;     // n x p  G V
+  const double* theta;
+  double* res;       // kmax
+  int n, p, kmax;
+};
+
+// one warp per (matrix, wanted Ritz pair): r_t = || W[:, t] - theta_t V[:, t] ||
+__global__ void ritz_residual(const ResDev* P, int nprob, int maxk) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int b = gw / maxk, t = gw % maxk;
+  if (b >= nprob) return;
+  const ResDev& R = P[b];
+  if (t >= R.kmax) return;
+  const double th = R.theta[t];
+  double s = 0.0;
+  for (int i = lane; i < R.n; i += 32) {
+    const cplx w = R.W[(long long)i * R.p + t], v = R.V[(long long)i * R.p + t];
+    const double dx = w.x - th * v.x, dy = w.y - th * v.y;
+    s += dx * dx + dy * dy;
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) R.res[t] = sqrt(s);
+}
+
+struct FinDev {
+  const cplx* G;
+  const cplx* V;     // n x p
+  const double* theta;
+  HeevProblem hp;    // destination (lam, Vt, k_out, w_out, tol2, floor_rel, max_bond)
+  int p;
+};
+
+// trace, truncation decision and discarded weight (one thread per matrix), then Vt = V^T rows
+__global__ void large_finish(FinDev* P, int nprob) {
+  const int b = blockIdx.y;
+  if (b >= nprob) return;
+  const FinDev& F = P[b];
+  const HeevProblem& H = F.hp;
+  const int n = H.n, kmax = H.kmax;
+  __shared__ double red[32];
+  double tr = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tr += F.G[(long long)i * n + i].x;
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = tr;
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double trace = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) trace += red[w];
+    const double l1 = F.theta[0];
+    int k = 1;
+    double kept = 0.0;
+    if (trace > 0.0 && l1 > 0.0) {
+      int cnt = 0;
+      for (int t = 0; t < kmax; ++t)
+        if (F.theta[t] > H.tol2 * l1 && F.theta[t] > H.floor_rel * l1) ++cnt;
+      k = cnt < 1 ? 1 : (cnt > H.max_bond ? H.max_bond : cnt);
+      for (int t = 0; t < k; ++t) kept += F.theta[t];
+    }
+    for (int t = 0; t < kmax; ++t) H.lam[t] = (t < k && trace > 0.0 && l1 > 0.0) ? F.theta[t] : 0.0;
+    if (H.k_out) *H.k_out = k;
+    if (H.w_out) *H.w_out = fmax(trace - kept, 0.0);
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)kmax * n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(i / n), r = (int)(i % n);
+    H.Vt[i] = F.V[(long long)r * F.p + t];
+  }
+}
+
+// scaled Chebyshev filter value p_m(x) on [lo, cut] normalised at top (host scalar recurrence,
+// identical to the one applied to the vectors)
+double cheb_value(double x, int m, double lo, double cut, double top) {
+  const double e = 0.5 * (cut - lo), c = 0.5 * (cut + lo);
+  const double s1 = e / (top - c);
+  double sigma = s1;
+  double y0 = 1.0, y1 = (x - c) * s1 / e;
+  for (int j = 2; j <= m; ++j) {
+    const double sn = 1.0 / (2.0 / s1 - sigma);
+    const double y2 = 2.0 * sn / e * (x - c) * y1 - sigma * sn * y0;
+    y0 = y1;
+    y1 = y2;
+    sigma = sn;
+  }
+  return y1;
+}
+
+struct Job {
+  HeevProblem* hp;
+  int n, p, kmax;
+  cplx *Gs, *V, *Y, *W, *V2, *W2, *H, *Zt, *Wg, *Li, *Q1, *tau;
+  double *theta, *res, *dscale, *hwork;
+  int* info;
+  bool done = false;
+};
+
+}  // namespace
+
+bool chfsi_applicable(int n, int kmax) {
+  const int p = chfsi_block(n, kmax);
+  return n > kLargeN && p <= 512 && 2 * p <= n;
+}
+
+int chfsi_block(int n, int kmax) {
+  int p = kmax + std::max(32, kmax / 2);
+  p = (p + 15) / 16 * 16;
+  return std::min(p, n);
+}
+
+void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st) {
+  if (probs.empty()) return;
+  cudaStream_t s = ctx->stream;
+  const int nb = (int)probs.size();
+  std::vector<Job> J(nb);
+  auto A = [&](size_t elems) { return static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * std::max<size_t>(elems, 1))); };
+  auto Ad = [&](size_t elems) { return static_cast<double*>(ctx->scratch.alloc(sizeof(double) * std::max<size_t>(elems, 1))); };
+  int maxk = 0;
+  for (int b = 0; b < nb; ++b) {
+    Job& j = J[b];
+    j.hp = probs[b];
+    j.n = j.hp->n;
+    j.kmax = j.hp->kmax;
+    j.p = chfsi_block(j.n, j.kmax);
+    const size_t n = j.n, p = j.p;
+    j.Gs = A(n * n);
+    j.V = A(n * p); j.Y = A(n * p); j.W = A(n * p); j.V2 = A(n * p); j.W2 = A(n * p); j.Q1 = A(n * p);
+    j.H = A(p * p); j.Zt = A(p * p); j.Wg = A(p * p); j.Li = A(p * p);
+    j.tau = A(std::max(n, p));
+    j.theta = Ad(p); j.res = Ad(j.kmax); j.dscale = Ad(p);
+    j.hwork = Ad(heev_work_doubles((int)p, (int)p));
+    j.info = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * 2));
+    maxk = std::max(maxk, j.kmax);
+  }
+  auto large_launch = [&](void (*kern)(LargeDev*), std::vector<Job*>& act, std::vector<double>* shifts, bool scale) {
+    std::vector<LargeDev> L;
+    for (size_t q = 0; q < act.size(); ++q) {
+      Job& j = *act[q];
+      L.push_back(LargeDev{j.hp->A, j.Gs, j.V, j.dscale, shifts ? (*shifts)[q] : 0.0, j.n, j.p});
+    }
+    LargeDev* d = static_cast<LargeDev*>(ctx->stager->put(L.data(), sizeof(LargeDev) * L.size()));
+    (void)scale;
+    kern<<<dim3(296, (unsigned)L.size()), 256, 0, s>>>(d);
+    count_launch();
+  };
+  // orthonormalise V (n x p) of every active job in place: shifted CholeskyQR3 (Fukaya et al.):
+  // a first Cholesky pass of V^H V + s I (s ~ 1e-13 max diag) brings any block with
+  // cond <= ~1e13 to cond <= ~1e7, then CholeskyQR2 finishes; V keeps its span throughout.
+  auto orth = [&](std::vector<Job*>& act) {
+    for (int pass = 0; pass < 3; ++pass) {
+      std::vector<GemmProblem> g1, g2;
+      std::vector<PotrfProblem> p1;
+      std::vector<TrtriProblem> t1;
+      for (Job* jp : act) {
+        Job& j = *jp;
+        const int64_t n = j.n, p = j.p;
+        g1.push_back(mk_gemm(j.V, OP_C, p, j.V, OP_N, p, j.Wg, p, p, p, n));
+        PotrfProblem pp{j.Wg, p, (int)p, 0, j.info + (pass == 2 ? 1 : 0), pass == 0 ? 1e-15 : 1e-14};
+        pp.shift_rel = pass == 0 ? 1e-13 : 0.0;
+        p1.push_back(pp);
+        t1.push_back(TrtriProblem{j.Wg, j.Li, p, (int)p, 0});
+        g2.push_back(mk_gemm(j.V, OP_N, p, j.Li, OP_C, p, j.Q1, p, n, p, p));
+      }
+      gemm_batch(ctx, g1, st);
+      launch_potrf(p1.data(), (int)p1.size(), *ctx->stager, s);
+      launch_trtri(t1.data(), (int)t1.size(), *ctx->stager, s);
+      gemm_batch(ctx, g2, st);
+      for (Job* jp : act) std::swap(jp->V, jp->Q1);
+    }
+  };
+  // Rayleigh-Ritz of every active job: theta, V <- V Z (W <- G V Z), residuals of wanted pairs
+  auto rayleigh_ritz = [&](std::vector<Job*>& act) {
+    std::vector<GemmProblem> gw, gh, gv;
+    std::vector<HeevProblem> hh;
+    std::vector<ResDev> rd;
+    for (Job* jp : act) {
+      Job& j = *jp;
+      const int64_t n = j.n, p = j.p;
+      gw.push_back(mk_gemm(j.hp->A, OP_N, n, j.V, OP_N, p, j.W, p, n, p, n));     // W = G V
+      gh.push_back(mk_gemm(j.V, OP_C, p, j.W, OP_N, p, j.H, p, p, p, n));         // H = V^H W
+      HeevProblem h{};
+      h.A = j.H; h.n = (int)p; h.kmax = (int)p; h.lam = j.theta; h.Vt = j.Zt; h.k_out = nullptr; h.w_out = nullptr;
+      h.work = j.hwork; h.tau = j.tau; h.tol2 = 0.0; h.floor_rel = -1e300; h.max_bond = (int)p;
+      hh.push_back(h);
+      gv.push_back(mk_gemm(j.V, OP_N, p, j.Zt, OP_T, p, j.V2, p, n, p, p));       // V2 = V Z
+      gv.push_back(mk_gemm(j.W, OP_N, p, j.Zt, OP_T, p, j.W2, p, n, p, p));       // W2 = W Z
+      rd.push_back(ResDev{j.V2, j.W2, j.theta, j.res, (int)n, (int)p, j.kmax});
+    }
+    gemm_batch(ctx, gw, st);
+    gemm_batch(ctx, gh, st);
+    launch_heev(hh.data(), (int)hh.size(), *ctx->stager, s);
+    gemm_batch(ctx, gv, st);
+    const ResDev* d = static_cast<const ResDev*>(ctx->stager->put(rd.data(), sizeof(ResDev) * rd.size()));
+    const long long warps = (long long)rd.size() * maxk;
+    ritz_residual<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(d, (int)rd.size(), maxk);
+    count_launch();
+    for (Job* jp : act) {
+      std::swap(jp->V, jp->V2);
+      std::swap(jp->W, jp->W2);
+    }
+  };
+
+  prof_begin(s);
+  std::vector<Job*> act;
+  for (auto& j : J) act.push_back(&j);
+  large_launch(random_fill, act, nullptr, false);
+  orth(act);
+  rayleigh_ritz(act);
+  int maxp = 0;
+  for (auto& j : J) maxp = std::max(maxp, j.p);
+  ctx->ensure_small(sizeof(double) * (size_t)nb * (maxp + maxk) + sizeof(int) * 2 * nb + 64);
+  double* hbuf = reinterpret_cast<double*>(ctx->hbuf);
+  int* hinfo = reinterpret_cast<int*>(hbuf + (size_t)nb * (maxp + maxk));
+  int iter = 0;
+  for (;; ++iter) {
+    for (int b = 0; b < nb; ++b) {
+      if (J[b].done) continue;
+      TTN_CUDA(cudaMemcpyAsync(hbuf + (size_t)b * (maxp + maxk), J[b].theta, sizeof(double) * J[b].p,
+                               cudaMemcpyDeviceToHost, s));
+      TTN_CUDA(cudaMemcpyAsync(hbuf + (size_t)b * (maxp + maxk) + maxp, J[b].res, sizeof(double) * J[b].kmax,
+                               cudaMemcpyDeviceToHost, s));
+      TTN_CUDA(cudaMemcpyAsync(hinfo + 2 * b, J[b].info, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+    }
+    ctx->sync();
+    act.clear();
+    std::vector<double> shifts;
+    std::vector<std::vector<double>> coefs;
+    for (int b = 0; b < nb; ++b) {
+      Job& j = J[b];
+      if (j.done) continue;
+      const double* th = hbuf + (size_t)b * (maxp + maxk);
+      const double* rs = th + maxp;
+      const double top = th[0];
+      if (hinfo[2 * b] != 0 || hinfo[2 * b + 1] != 0)
+        throw Error(TTN_ERR_NUMERIC, "large-Gram eigensolver: CholeskyQR2 of the filtered block flagged rank deficiency");
+      bool conv = true;
+      double worst = 0.0;
+      for (int t = 0; t < j.kmax; ++t) {
+        if (!std::isfinite(th[t]) || !std::isfinite(rs[t])) throw Error(TTN_ERR_NUMERIC, "non-finite Ritz pair (non-finite input?)");
+        if (th[t] <= 1e-13 * top) break;   // numerically-zero directions are never kept (reading A4)
+        worst = std::max(worst, rs[t]);
+        if (rs[t] > kResTol * top) conv = false;
+      }
+      if (!(top > 0.0)) conv = true;   // zero Gram: nothing to resolve
+      if (conv) { j.done = true; continue; }
+      if (iter >= kMaxIter) {
+        if (worst <= 1e-9 * top) { j.done = true; continue; }
+        throw Error(TTN_ERR_NUMERIC, "large-Gram eigensolver did not converge (residual " + std::to_string(worst / top) + ")");
+      }
+      // damp [lo, cut]: cut = smallest Ritz value (>= a tiny fraction of top), lo just below 0
+      const double cut = std::max(th[j.p - 1], 1e-6 * top), lo = -1e-12 * top;
+      // degree: amplify the slowest wanted direction by ~1e8 per pass (8 <= m <= 40)
+      int m = 8;
+      const double xk = th[std::min(j.kmax, j.p) - 1];
+      while (m < 40 && std::fabs(cheb_value(xk, m, lo, cut, top)) < 1e8 * std::fabs(cheb_value(cut, m, lo, cut, top)))
+        m += 4;
+      std::vector<double> cf;   // m, lo, cut, top
+      cf.push_back(m); cf.push_back(lo); cf.push_back(cut); cf.push_back(top);
+      coefs.push_back(cf);
+      // column pre-scaling D = diag(1 / p_m(theta_j))
+      std::vector<double> dsc(j.p);
+      for (int t = 0; t < j.p; ++t) {
+        const double v = cheb_value(th[t], m, lo, cut, top);
+        dsc[t] = (std::fabs(v) > 1e-12) ? 1.0 / v : (v < 0 ? -1e12 : 1e12);   // cap the dynamic range
+      }
+      TTN_CUDA(cudaMemcpyAsync(j.dscale, ctx->stager->put(dsc.data(), sizeof(double) * j.p), sizeof(double) * j.p,
+                               cudaMemcpyDeviceToDevice, s));
+      shifts.push_back(0.5 * (cut + lo));
+      act.push_back(&j);
+    }
+    if (act.empty()) break;
+    large_launch(shift_copy, act, &shifts, false);
+    large_launch(col_scale, act, nullptr, true);
+    // filter: Y = p_m(G) V, recurrence over (X, Y) with X = V, in place
+    int mmax = 0;
+    for (auto& cf : coefs) mmax = std::max(mmax, (int)cf[0]);
+    std::vector<double> sigma(act.size()), s1(act.size());
+    {
+      std::vector<GemmProblem> g;
+      for (size_t q = 0; q < act.size(); ++q) {
+        Job& j = *act[q];
+        const double lo = coefs[q][1], cut = coefs[q][2], top = coefs[q][3];
+        const double e = 0.5 * (cut - lo), c = 0.5 * (cut + lo);
+        s1[q] = e / (top - c);
+        sigma[q] = s1[q];
+        GemmProblem gp = mk_gemm(j.Gs, OP_N, j.n, j.V, OP_N, j.p, j.Y, j.p, j.n, j.p, j.n);
+        gp.alpha = make_double2(s1[q] / e, 0.0);
+        g.push_back(gp);
+      }
+      gemm_batch(ctx, g, st);
+    }
+    for (int deg = 2; deg <= mmax; ++deg) {
+      std::vector<GemmProblem> g;
+      for (size_t q = 0; q < act.size(); ++q) {
+        Job& j = *act[q];
+        if (deg > (int)coefs[q][0]) continue;
+        const double lo = coefs[q][1], cut = coefs[q][2];
+        const double e = 0.5 * (cut - lo);
+        const double sn = 1.0 / (2.0 / s1[q] - sigma[q]);
+        // X <- (2 sn / e) Gs Y - sigma sn X   (X = V buffer), then swap roles
+        GemmProblem gp = mk_gemm(j.Gs, OP_N, j.n, j.Y, OP_N, j.p, j.V, j.p, j.n, j.p, j.n);
+        gp.alpha = make_double2(2.0 * sn / e, 0.0);
+        gp.beta = make_double2(-sigma[q] * sn, 0.0);
+        g.push_back(gp);
+        sigma[q] = sn;
+        std::swap(j.V, j.Y);
+      }
+      gemm_batch(ctx, g, st);
+    }
+    // filtered block is in Y
+    for (Job* jp : act) std::swap(jp->V, jp->Y);
+    orth(act);
+    rayleigh_ritz(act);
+  }
+  // results in the HeevProblem contract
+  std::vector<FinDev> F;
+  for (auto& j : J) F.push_back(FinDev{j.hp->A, j.V, j.theta, *j.hp, j.p});
+  FinDev* d = static_cast<FinDev*>(ctx->stager->put(F.data(), sizeof(FinDev) * F.size()));
+  large_finish<<<dim3(64, nb), 256, 0, s>>>(d, nb);
+  count_launch();
+  double fl = 0.0;
+  for (auto& j : J) fl += 8.0 * (double)j.n * j.n * j.p * (iter + 2);
+  prof_end(s, "heev_large", fl, 0.0);
+  (void)iter;
+}
+
+}  // namespace tcbc

@@ -50,6 +50,12 @@ __global__ void __launch_bounds__(256) potrf_grouped(const PotrfProblem* __restr
   double md = -1e300;
   for (int i = threadIdx.x; i < n; i += blockDim.x) md = fmax(md, A[i * ld + i].x);
   md = block_max(md, red);
+  if (P.shift_rel > 0.0 && md > 0.0) {
+    const double sh = P.shift_rel * md;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) A[i * ld + i].x += sh;
+    md += sh;
+    __syncthreads();
+  }
   const double thresh = P.rel_tol * md;
   if (threadIdx.x == 0) s_fail = (md > 0.0 && isfinite(md)) ? 0 : 1;
   __syncthreads();

@@ -9,13 +9,18 @@
 //
 // sm_100a has no tcgen05 kind::f64: FP64 tensor-core math is the warp-level
 // mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Measured peak on this pool: 37.1 TF/s
-// (profiles/fp64_peaks_r01.json).  One DMMA = 256 FMAs, so an SM retires one DMMA per
-// ~4 clocks: the kernel needs register blocking (warp tiles of 4x4 or 4x2 / 2x8 DMMA tiles)
-// more than shared-memory bandwidth.  Complex product by the 4M rule on separate re/im
-// accumulators:  Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br.
-// Operands are staged in shared memory by a 3-stage cp.async (16 B per complex) pipeline;
-// shared-memory layouts are chosen per problem (k-contiguous or m/n-contiguous legs) so the
-// global loads coalesce whenever one leg of the operand has unit stride.
+// (profiles/fp64_peaks_r01.json) = one DMMA per 16 clocks per SM sub-partition; the same
+// microbenchmark shows that 2 warps per sub-partition with 8 independent accumulator chains
+// each saturate it.  So the kernel is organised around (i) independent DMMA chains: a warp
+// tile of 4x4 (or 4x2) 8x8 tiles, and the four real products of the complex 4M rule
+//   Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br
+// issued pass by pass (each accumulator is touched once per 16/32 DMMAs, never back to back),
+// (ii) fragments of both k-steps of a stage read from shared memory before the first DMMA,
+// (iii) no integer division in the k loop: the multi-index -> offset decode of the k legs is
+// done one stage ahead by 2*BK threads into a small shared-memory ring (rows / columns are
+// decoded once per CTA).  Operands are staged by a 3-stage cp.async (16 B = one complex)
+// pipeline; shared-memory layouts are chosen per problem (k-contiguous or m/n-contiguous legs)
+// so the global loads coalesce whenever one leg of the operand has unit stride.
 #include "kernels.h"
 #include "prof.h"
 #include <algorithm>
@@ -33,7 +38,7 @@ template <int BM, int BN, bool AKM, bool BNM>
 struct Cfg {
   static constexpr int A_ELEMS = AKM ? BK * BM : BM * PADK;
   static constexpr int B_ELEMS = BNM ? BN * PADK : BK * BN;
-  static constexpr int TAB = (2 * BM + 2 * BN) * 8;
+  static constexpr int TAB = (2 * BM + 2 * BN + 2 * STAGES * BK) * 8;
   static constexpr int BYTES = STAGES * (A_ELEMS + B_ELEMS) * 16 + TAB + 1024;
 };
 
@@ -46,22 +51,30 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Not volatile: the accumulator operands carry the dependencies, so ptxas may interleave the
+// fragment loads of the next k-step with these.
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 
-// offset of multi-index x in a group of n legs (row-major: last leg fastest)
+// sign flip on the integer pipe (keeps the FP64 pipe out of the inner loop)
+__device__ __forceinline__ double neg_if(double x, bool neg) {
+  return neg ? __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x)) : x;
+}
+
+// offset of multi-index x in a group of n legs (row-major: last leg fastest); the outermost
+// leg needs no division
 __device__ __forceinline__ long long goff(int x, int n, const int* d, const long long* s) {
   long long off = 0;
 #pragma unroll 1
-  for (int i = n - 1; i >= 0; --i) {
+  for (int i = n - 1; i >= 1; --i) {
     int q = x / d[i];
     off += (long long)(x - q * d[i]) * s[i];
     x = q;
   }
-  return off;
+  return off + (long long)x * s[0];
 }
 
 __device__ __forceinline__ int find_problem(const GemmProblem* p, int n, int tile) {
@@ -74,11 +87,12 @@ __device__ __forceinline__ int find_problem(const GemmProblem* p, int n, int til
 }
 
 template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
-__global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob) {
+__global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob) {
   using C_ = Cfg<BM, BN, AKM, BNM>;
   constexpr int WTM = BM / WGM, WTN = BN / WGN;     // warp tile
   constexpr int TM = WTM / 8, TN = WTN / 8;         // DMMA tiles per warp
   static_assert(WGM * WGN == THREADS / 32, "warp grid");
+  static_assert((BM * BK) % THREADS == 0 && (BN * BK) % THREADS == 0, "load mapping");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
   cplx* Bs = As + STAGES * C_::A_ELEMS;
@@ -86,7 +100,9 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
   long long* colB = rowA + BM;
   long long* rowC = colB + BN;
   long long* colC = rowC + BM;
-  GemmProblem* sP = reinterpret_cast<GemmProblem*>(colC + BN);
+  long long* kA = colC + BN;                 // [STAGES][BK] k-leg offsets into A (-1: k >= K)
+  long long* kB = kA + STAGES * BK;          // [STAGES][BK] k-leg offsets into B
+  GemmProblem* sP = reinterpret_cast<GemmProblem*>(kB + STAGES * BK);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) *sP = probs[find_problem(probs, nprob, blockIdx.x)];
@@ -105,24 +121,37 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
     colB[i] = n < N ? goff(n, P.nn, P.nd, P.bn) : -1;
     colC[i] = n < N ? goff(n, P.nn, P.nd, P.cn) : -1;
   }
+  const int ktiles = (K + BK - 1) / BK;
+  // k-leg offsets of tile T into ring slot T % STAGES (thread j < 2*BK: operand j / BK, k j % BK)
+  auto k_offsets = [&](int T, int j) {
+    const int slot = T % STAGES, kl = j % BK, k = T * BK + kl;
+    if (j < BK) kA[slot * BK + kl] = k < K ? goff(k, P.nk, P.kd, P.ak) : -1;
+    else kB[slot * BK + kl] = k < K ? goff(k, P.nk, P.kd, P.bk) : -1;
+  };
+  for (int j = tid; j < 2 * BK * STAGES; j += THREADS) {
+    const int T = j / (2 * BK);
+    if (T < ktiles) k_offsets(T, j % (2 * BK));
+  }
   __syncthreads();
   const cplx* __restrict__ Ag = P.A;
   const cplx* __restrict__ Bg = P.B;
   const int wm = (warp / WGN) * WTM, wn = (warp % WGN) * WTN;
   const bool conjA = P.conjA != 0, conjB = P.conjB != 0;
 
-  auto load_stage = [&](int stage, int k0) {
+  auto load_stage = [&](int T) {
+    const int stage = T % STAGES;
     cplx* as = As + stage * C_::A_ELEMS;
     cplx* bs = Bs + stage * C_::B_ELEMS;
+    const long long* ka = kA + stage * BK;
+    const long long* kb = kB + stage * BK;
     if (!AKM) {   // As[m][k]: k fixed per thread
       const int k = tid % BK;
-      const bool kv = k0 + k < K;
-      const long long ko = kv ? goff(k0 + k, P.nk, P.kd, P.ak) : 0;
+      const long long ko = ka[k];
 #pragma unroll
       for (int r = 0; r < (BM * BK) / THREADS; ++r) {
         const int m = tid / BK + r * (THREADS / BK);
         const long long ro = rowA[m];
-        const bool v = kv && ro >= 0;
+        const bool v = ko >= 0 && ro >= 0;
         cp_async16(as + m * PADK + k, v ? Ag + ro + ko : Ag, v);
       }
     } else {      // As[k][m]
@@ -130,22 +159,19 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
       for (int r = 0; r < (BM * BK) / THREADS; ++r) {
         const int idx = tid + r * THREADS;
         const int k = idx / BM, m = idx % BM;
-        const bool kv = k0 + k < K;
-        const long long ro = rowA[m];
-        const bool v = kv && ro >= 0;
-        const long long ko = v ? goff(k0 + k, P.nk, P.kd, P.ak) : 0;
+        const long long ro = rowA[m], ko = ka[k];
+        const bool v = ko >= 0 && ro >= 0;
         cp_async16(as + k * BM + m, v ? Ag + ro + ko : Ag, v);
       }
     }
     if (BNM) {    // Bs[n][k]: k fixed per thread
       const int k = tid % BK;
-      const bool kv = k0 + k < K;
-      const long long ko = kv ? goff(k0 + k, P.nk, P.kd, P.bk) : 0;
+      const long long ko = kb[k];
 #pragma unroll
       for (int r = 0; r < (BN * BK) / THREADS; ++r) {
         const int n = tid / BK + r * (THREADS / BK);
         const long long co = colB[n];
-        const bool v = kv && co >= 0;
+        const bool v = ko >= 0 && co >= 0;
         cp_async16(bs + n * PADK + k, v ? Bg + co + ko : Bg, v);
       }
     } else {      // Bs[k][n]
@@ -153,10 +179,8 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
       for (int r = 0; r < (BN * BK) / THREADS; ++r) {
         const int idx = tid + r * THREADS;
         const int k = idx / BN, n = idx % BN;
-        const bool kv = k0 + k < K;
-        const long long co = colB[n];
-        const bool v = kv && co >= 0;
-        const long long ko = v ? goff(k0 + k, P.nk, P.kd, P.bk) : 0;
+        const long long co = colB[n], ko = kb[k];
+        const bool v = ko >= 0 && co >= 0;
         cp_async16(bs + k * BN + n, v ? Bg + co + ko : Bg, v);
       }
     }
@@ -171,10 +195,9 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
       acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
     }
 
-  const int ktiles = (K + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_stage(s, s * BK);
+    if (s < ktiles) load_stage(s);
     cp_async_commit();
   }
 
@@ -182,40 +205,54 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped(const GemmProblem* __re
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
+    // decode the k legs of tile kt + STAGES (slot kt % STAGES: its last reader, the load of
+    // tile kt, was issued before this barrier); visible to the loads after the next barrier
+    if (tid < 2 * BK && kt + STAGES < ktiles) k_offsets(kt + STAGES, tid);
     {
       const int kn = kt + STAGES - 1;
-      if (kn < ktiles) load_stage(kn % STAGES, kn * BK);
+      if (kn < ktiles) load_stage(kn);
       cp_async_commit();
     }
     const cplx* as = As + (kt % STAGES) * C_::A_ELEMS;
     const cplx* bs = Bs + (kt % STAGES) * C_::B_ELEMS;
+    double ar[BK / 4][TM], ai[BK / 4][TM], nai[BK / 4][TM], br[BK / 4][TN], bi[BK / 4][TN];
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double ar[TM], ai[TM], nai[TM], br[TN], bi[TN];
+    for (int q = 0; q < BK / 4; ++q) {
+      const int k = q * 4 + fc;
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        const int m = wm + i * 8 + fr, k = kk + fc;
+        const int m = wm + i * 8 + fr;
         const cplx a = AKM ? as[k * BM + m] : as[m * PADK + k];
-        ar[i] = a.x;
-        ai[i] = conjA ? -a.y : a.y;
-        nai[i] = -ai[i];
+        ar[q][i] = a.x;
+        ai[q][i] = neg_if(a.y, conjA);
+        nai[q][i] = neg_if(a.y, !conjA);
       }
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
-        const int n = wn + j * 8 + fr, k = kk + fc;
+        const int n = wn + j * 8 + fr;
         const cplx b = BNM ? bs[n * PADK + k] : bs[k * BN + n];
-        br[j] = b.x;
-        bi[j] = conjB ? -b.y : b.y;
+        br[q][j] = b.x;
+        bi[q][j] = neg_if(b.y, conjB);
       }
+    }
+#pragma unroll
+    for (int q = 0; q < BK / 4; ++q) {
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          dmma(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
-          dmma(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
-          dmma(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
-          dmma(acc_im[i][j][0], acc_im[i][j][1], ai[i], br[j]);
-        }
+        for (int j = 0; j < TN; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], ar[q][i], br[q][j]);
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], ar[q][i], bi[q][j]);
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], nai[q][i], bi[q][j]);
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], ai[q][i], br[q][j]);
     }
   }
   cp_async_wait<0>();
@@ -286,6 +323,19 @@ void launch_shape(std::vector<GemmProblem>* g4, Stager& st, cudaStream_t s) {
   launch_variant<BM, BN, WGM, WGN, true, true>(g4[3], st, s);
 }
 
+// CTA tile shapes (BM x BN); warp tiles 32x32 except the 16-wide skinny shapes (32x16, 16x32)
+struct TileShape { int bm, bn; double eff; };
+constexpr TileShape kShapes[] = {{64, 64, 1.0}, {128, 32, 1.0}, {32, 128, 1.0}, {128, 16, 0.8}, {16, 128, 0.8}};
+constexpr int kNumShapes = 5;
+
+// estimated cost of a problem on a tile shape: padded DMMA work / relative warp-tile efficiency
+double shape_cost(const GemmProblem& p, const TileShape& t) {
+  const double mp = (double)((p.M + t.bm - 1) / t.bm) * t.bm;
+  const double np = (double)((p.N + t.bn - 1) / t.bn) * t.bn;
+  const double kp = (double)((p.K + BK - 1) / BK) * BK;
+  return mp * np * kp / t.eff;
+}
+
 }  // namespace
 
 void gemm_from_ops(GemmProblem& g, int opA, long long lda, int opB, long long ldb, long long ldc) {
@@ -302,8 +352,8 @@ void gemm_from_ops(GemmProblem& g, int opA, long long lda, int opB, long long ld
 }
 
 void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s) {
-  // group by tile shape (skinny N / skinny M / square) and shared-memory layouts
-  std::vector<GemmProblem> sq[4], tall[4], wide[4];
+  // group by tile shape (least padded work) and shared-memory layouts
+  std::vector<GemmProblem> by[kNumShapes][4];
   for (int i = 0; i < n; ++i) {
     GemmProblem p = h[i];
     if (p.M <= 0 || p.N <= 0) continue;
@@ -312,13 +362,19 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s) {
     // B: n-major smem when the innermost k leg is unit-stride and the innermost n leg is not
     const bool bnm = (p.bn[p.nn - 1] != 1) && (p.bk[p.nk - 1] == 1);
     const int v = (akm ? 2 : 0) + (bnm ? 1 : 0);
-    if (p.N <= 16 && p.M > 16) tall[v].push_back(p);
-    else if (p.M <= 16 && p.N > 16) wide[v].push_back(p);
-    else sq[v].push_back(p);
+    int best = 0;
+    double bc = shape_cost(p, kShapes[0]);
+    for (int t = 1; t < kNumShapes; ++t) {
+      const double c = shape_cost(p, kShapes[t]);
+      if (c < bc * 0.999) { bc = c; best = t; }
+    }
+    by[best][v].push_back(p);
   }
-  launch_shape<64, 64, 2, 2>(sq, st, s);
-  launch_shape<128, 16, 4, 1>(tall, st, s);
-  launch_shape<16, 128, 1, 4>(wide, st, s);
+  launch_shape<64, 64, 2, 2>(by[0], st, s);
+  launch_shape<128, 32, 4, 1>(by[1], st, s);
+  launch_shape<32, 128, 1, 4>(by[2], st, s);
+  launch_shape<128, 16, 4, 1>(by[3], st, s);
+  launch_shape<16, 128, 1, 4>(by[4], st, s);
 }
 
 }  // namespace tcbc

@@ -71,7 +71,8 @@ size_t heev_work_doubles(int n, int kmax);
 size_t heev_smem_bytes(int n, int kmax);
 int heev_max_n();
 
-// In-place lower Cholesky A = L L^H of an n x n Hermitian matrix (full storage, ld = lda);
+// In-place lower Cholesky A + s I = L L^H of an n x n Hermitian matrix (full storage, ld = lda;
+// s = shift_rel * max diag, 0 by default: the shifted first pass of CholeskyQR3);
 // the strict upper triangle is zeroed.  info = 0 or j+1 at the first pivot <= rel_tol * max diag.
 struct PotrfProblem {
   cplx* A;
@@ -80,6 +81,7 @@ struct PotrfProblem {
   int pad_;
   int* info;
   double rel_tol;
+  double shift_rel;
 };
 
 // Linv = L^{-1} (n x n lower, full storage, upper zeroed).

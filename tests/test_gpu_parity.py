@@ -218,3 +218,55 @@ def test_config5_circuit_layers(P, ctx):
         d_cos, d_rel = distances(g, po)
         assert d_cos <= 1e-10 and d_rel <= 1e-6, (d_cos, d_rel)
         assert g.bonds() == po.bonds()
+
+
+@pytest.mark.parametrize("mb", [64, 96])
+def test_large_gram_chebyshev_eigensolver(P, ctx, mb):
+    """Compress Grams of order 768 > 512 go through the Chebyshev-filtered subspace solver
+    (csrc/chfsi.cu).  Root d=128 with two d=8 leaves, chi=64, D=12: the down-sweep Grams are
+    768 x 768 with a flat spectrum at the cut (lambda_64/lambda_65 ~ 1.005), so the kept
+    subspace must be resolved to ~1e-10 to meet the parity bound."""
+    inst = W.configs.random_instance([-1, 0, 0], [128, 8, 8], 64, 12, mb, seed=11)
+    phi_g, phi_o, rep, op_o, psi_o = _run(P, ctx, inst)
+    d_cos, d_rel = distances(phi_g, phi_o)
+    assert d_cos <= 1e-10, (d_cos, d_rel)
+    # A19 sufficient condition (|O psi|^2 would need a 768-wide dense product here)
+    assert abs(norm(phi_g) ** 2 - norm(phi_o) ** 2) <= 1e-10 * norm(phi_o) ** 2
+    assert phi_g.bonds() == phi_o.bonds()
+    assert rep["discarded_weight_sum"] > 0.0
+    for i, t in enumerate(phi_g.tensors):
+        if i == phi_g.root:
+            continue
+        q = np.moveaxis(t, 1, -1).reshape(-1, t.shape[1])
+        assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
+
+
+def test_config4_t3ns_matches_oracle_golden(P, ctx):
+    """BASELINE config 4 (reading A12: 67-node T3NS, chi=128, D=16, max_bond=128) at full size.
+    The oracle needs ~6 min on 8 cores, so its results are stored by tests/golden/make_golden.py
+    (calls only oracle/): bonds, ||phi||^2 and every compress rank.  With the oracle's output
+    tensors present (tests/golden/cfg4_seed0_phi.npz, 88 MB, not in git) the gauge-invariant
+    distance is checked too."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg4_seed0.json")))
+    inst = W.make_config(4, seed=0)
+    op_g, st_g = gpu_pair(P, ctx, inst)
+    out, rep = P.cbc_apply(ctx, op_g, st_g, inst.max_bond)
+    phi_g = to_oracle(P, out, inst.parent)
+    assert phi_g.bonds() == gold["bonds"]
+    n2 = norm(phi_g) ** 2
+    assert abs(n2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"], (n2, gold["phi_norm2"])
+    assert abs(rep["norm"] ** 2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"]
+    for i, t in enumerate(phi_g.tensors):       # P3
+        if i == phi_g.root:
+            continue
+        q = np.moveaxis(t, 1, -1).reshape(-1, t.shape[1])
+        assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
+    npz = os.path.join(os.path.dirname(__file__), "golden", "cfg4_seed0_phi.npz")
+    if os.path.exists(npz):
+        z = np.load(npz)
+        phi_o = TTN(inst.parent, [z[f"arr_{i}"] for i in range(len(inst.parent))], "state")
+        d_cos, d_rel = distances(phi_g, phi_o)
+        print(f"config 4 full parity: 1-cos={d_cos:.3e} rel={d_rel:.3e}")
+        assert d_cos <= 1e-10, (d_cos, d_rel)
