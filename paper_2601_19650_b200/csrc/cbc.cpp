@@ -107,8 +107,9 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     cplx* G = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
     GemmProblem g = (m >= n) ? mk_gemm(J.X, OP_C, n, J.X, OP_N, n, G, nn, n, n, m)     // G = X^H X
                              : mk_gemm(J.X, OP_N, n, J.X, OP_C, n, G, nn, m, m, n);    // K = X X^H
+    g.sym = 1;   // Hermitian: lower tiles + mirror (HERK)
     grams.push_back(g);
-    flops_inst[J.inst] += 8.0 * (double)g.M * g.N * g.K;
+    flops_inst[J.inst] += gemm_flops(g);
     HeevProblem& h = hp[j];
     h.A = G;
     h.n = (int)nn;
@@ -234,10 +235,12 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
       return g;
     };
     g1.push_back(gp(J.S, OP_C, k, J.S, OP_N, k, W, k, k, m));        // W = S^H S
+    g1.back().sym = 1;
     p1.push_back(PotrfProblem{W, k, (int)k, 0, d_info + 2 * j, kCholTol});
     t1.push_back(TrtriProblem{W, Li, k, (int)k, 0});
     g2.push_back(gp(J.S, OP_N, k, Li, OP_C, k, Q1, m, k, k));        // Q1 = S L^{-H}
     g3.push_back(gp(Q1, OP_C, k, Q1, OP_N, k, W2, k, k, m));         // W2 = Q1^H Q1
+    g3.back().sym = 1;
     p2.push_back(PotrfProblem{W2, k, (int)k, 0, d_info + 2 * j + 1, kCholTol * 1e-2});
     t2.push_back(TrtriProblem{W2, Li2, k, (int)k, 0});
     g4.push_back(gp(Q1, OP_N, k, Li2, OP_C, k, J.Q, m, k, k));       // Q = Q1 L2^{-H}

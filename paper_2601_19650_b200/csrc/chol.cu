@@ -10,6 +10,7 @@
 // spread over the CTA.
 #include "kernels.h"
 #include "prof.h"
+#include <algorithm>
 #include <cmath>
 
 namespace tcbc {
@@ -40,76 +41,211 @@ __device__ double block_max(double v, double* red) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) potrf_grouped(const PotrfProblem* __restrict__ probs) {
+constexpr int CH_NB = 16;      // panel / row-block width
+constexpr int CH_THREADS = 512;
+
+// Blocked right-looking Cholesky (lower): for each 16-column panel, (1) the panel is staged in
+// shared memory, (2) its 16 x 16 diagonal block is factored by one warp (lane = row),
+// (3) the rows below are solved against L11^H (thread per row), (4) the panel is written back
+// and the trailing lower triangle is updated once per panel (A22 -= P P^H) with 4 x 4 register
+// tiles reading the staged panel (16 complex MACs per element per panel instead of one
+// global read-modify-write per column).  One CTA per matrix.
+__global__ void __launch_bounds__(CH_THREADS) potrf_grouped(const PotrfProblem* __restrict__ probs) {
   const PotrfProblem P = probs[blockIdx.x];
   const int n = P.n;
   const long long ld = P.lda;
   cplx* A = P.A;
+  extern __shared__ __align__(16) unsigned char ch_smem[];
+  cplx* Pn = reinterpret_cast<cplx*>(ch_smem);   // [n][CH_NB]
   __shared__ double red[32];
   __shared__ int s_fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double md = -1e300;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) md = fmax(md, A[i * ld + i].x);
+  for (int i = tid; i < n; i += CH_THREADS) md = fmax(md, A[i * ld + i].x);
   md = block_max(md, red);
   if (P.shift_rel > 0.0 && md > 0.0) {
     const double sh = P.shift_rel * md;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) A[i * ld + i].x += sh;
+    for (int i = tid; i < n; i += CH_THREADS) A[i * ld + i].x += sh;
     md += sh;
-    __syncthreads();
   }
   const double thresh = P.rel_tol * md;
-  if (threadIdx.x == 0) s_fail = (md > 0.0 && isfinite(md)) ? 0 : 1;
+  if (tid == 0) s_fail = (md > 0.0 && isfinite(md)) ? 0 : 1;
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = 0; j < n && !s_fail; ++j) {
-    if (threadIdx.x == 0) {
-      double ajj = A[j * ld + j].x;
-      if (!(ajj > thresh) || !isfinite(ajj)) s_fail = j + 1;
-      else A[j * ld + j] = make_double2(sqrt(ajj), 0.0);
+  for (int j0 = 0; j0 < n && !s_fail; j0 += CH_NB) {
+    const int jb = min(CH_NB, n - j0), rows = n - j0;
+    for (int e = tid; e < rows * jb; e += CH_THREADS) {
+      const int r = e / jb, c = e % jb;
+      Pn[r * CH_NB + c] = A[(long long)(j0 + r) * ld + j0 + c];
+    }
+    __syncthreads();
+    if (warp == 0) {   // diagonal block, unblocked, lane = row
+      for (int c = 0; c < jb; ++c) {
+        if (lane == c) {
+          const double d = Pn[c * CH_NB + c].x;
+          if (!(d > thresh) || !isfinite(d)) s_fail = j0 + c + 1;
+          else Pn[c * CH_NB + c] = make_double2(sqrt(d), 0.0);
+        }
+        __syncwarp();
+        if (s_fail) break;
+        const double inv = 1.0 / Pn[c * CH_NB + c].x;
+        if (lane > c && lane < jb) {
+          const cplx v = Pn[lane * CH_NB + c];
+          Pn[lane * CH_NB + c] = make_double2(v.x * inv, v.y * inv);
+        }
+        __syncwarp();
+        if (lane > c && lane < jb) {
+          const cplx lc = Pn[lane * CH_NB + c];
+          for (int l = c + 1; l <= lane; ++l) {
+            const cplx u = cmulc(lc, Pn[l * CH_NB + c]);
+            Pn[lane * CH_NB + l].x -= u.x;
+            Pn[lane * CH_NB + l].y -= u.y;
+          }
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
     if (s_fail) break;
-    const double inv = 1.0 / A[j * ld + j].x;
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
-      cplx v = A[i * ld + j];
-      A[i * ld + j] = make_double2(v.x * inv, v.y * inv);
+    for (int r = jb + tid; r < rows; r += CH_THREADS) {   // x L11^H = p
+      cplx x[CH_NB];
+#pragma unroll
+      for (int c = 0; c < CH_NB; ++c) {
+        if (c >= jb) break;
+        cplx v = Pn[r * CH_NB + c];
+        for (int l = 0; l < c; ++l) {
+          const cplx u = cmulc(x[l], Pn[c * CH_NB + l]);
+          v.x -= u.x;
+          v.y -= u.y;
+        }
+        const double inv = 1.0 / Pn[c * CH_NB + c].x;
+        x[c] = make_double2(v.x * inv, v.y * inv);
+        Pn[r * CH_NB + c] = x[c];
+      }
     }
     __syncthreads();
-    for (int i = j + 1 + warp; i < n; i += nw) {
-      const cplx lij = A[i * ld + j];
-      for (int l = j + 1 + lane; l <= i; l += 32) {
-        cplx llj = A[l * ld + j];
-        cplx u = cmulc(lij, llj);
-        cplx a = A[i * ld + l];
-        A[i * ld + l] = make_double2(a.x - u.x, a.y - u.y);
+    for (int e = tid; e < rows * jb; e += CH_THREADS) {
+      const int r = e / jb, c = e % jb;
+      if (c <= r) A[(long long)(j0 + r) * ld + j0 + c] = Pn[r * CH_NB + c];
+    }
+    // trailing update on 4x4 tiles of the lower triangle of rows/cols [jb, rows)
+    const int t = rows - jb, tb = (t + 3) / 4;
+    const int ntiles = tb * (tb + 1) / 2;
+    for (int e = tid; e < ntiles; e += CH_THREADS) {
+      int bi = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (bi * (bi + 1) / 2 > e) --bi;
+      while ((bi + 1) * (bi + 2) / 2 <= e) ++bi;
+      const int bj = e - bi * (bi + 1) / 2;
+      const int r0 = jb + 4 * bi, l0 = jb + 4 * bj;
+      cplx acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
+      for (int c = 0; c < jb; ++c) {
+        cplx pr[4], pl[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          pr[a] = (r0 + a < rows) ? Pn[(r0 + a) * CH_NB + c] : make_double2(0.0, 0.0);
+          pl[a] = (l0 + a < rows) ? Pn[(l0 + a) * CH_NB + c] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const cplx u = cmulc(pr[a], pl[b]);
+            acc[a][b].x += u.x;
+            acc[a][b].y += u.y;
+          }
       }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int r = r0 + a, l = l0 + b;
+          if (r < rows && l <= r) {
+            cplx* p = A + (long long)(j0 + r) * ld + j0 + l;
+            p->x -= acc[a][b].x;
+            p->y -= acc[a][b].y;
+          }
+        }
     }
     __syncthreads();
   }
   __syncthreads();
   if (!s_fail) {
-    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+    for (long long e = tid; e < (long long)n * n; e += CH_THREADS) {
       int i = (int)(e / n), l = (int)(e % n);
       if (l > i) A[i * ld + l] = make_double2(0.0, 0.0);
     }
   }
-  if (threadIdx.x == 0 && P.info) *P.info = s_fail;
+  if (tid == 0 && P.info) *P.info = s_fail;
 }
 
-__global__ void __launch_bounds__(256) trtri_grouped(const TrtriProblem* __restrict__ probs) {
+// Blocked triangular inverse Linv = L^{-1} (lower), by 16-row blocks top to bottom: the block's
+// rows of L are staged in shared memory, one warp inverts the 16 x 16 diagonal block D, and
+// every column c < R0 is formed as  Linv[R, c] = -D^{-1} sum_{j in [c, R0)} L[R, j] Linv[j, c]
+// (thread per column, Linv rows already written read back coalesced).
+__global__ void __launch_bounds__(CH_THREADS) trtri_grouped(const TrtriProblem* __restrict__ probs) {
   const TrtriProblem P = probs[blockIdx.x];
   const int n = P.n;
   const long long ld = P.ld;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    for (int i = 0; i < c; ++i) P.Linv[i * ld + c] = make_double2(0.0, 0.0);
-    for (int i = c; i < n; ++i) {
-      cplx s = make_double2(i == c ? 1.0 : 0.0, 0.0);
-      for (int j = c; j < i; ++j) {
-        cplx u = cmul(P.L[i * ld + j], P.Linv[j * ld + c]);
-        s.x -= u.x;
-        s.y -= u.y;
-      }
-      P.Linv[i * ld + c] = cdiv(s, P.L[i * ld + i]);
+  extern __shared__ __align__(16) unsigned char ch_smem[];
+  cplx* Ls = reinterpret_cast<cplx*>(ch_smem);     // [CH_NB][n]
+  __shared__ cplx Dinv[CH_NB][CH_NB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int R0 = 0; R0 < n; R0 += CH_NB) {
+    const int rb = min(CH_NB, n - R0), w = R0 + rb;
+    for (int e = tid; e < rb * w; e += CH_THREADS) {
+      const int a = e / w, j = e % w;
+      Ls[a * n + j] = P.L[(long long)(R0 + a) * ld + j];
     }
+    __syncthreads();
+    if (warp == 0 && lane < rb) {   // column lane of D^{-1}: forward substitution
+      const int b = lane;
+      for (int a = 0; a < rb; ++a) {
+        cplx s = make_double2(a == b ? 1.0 : 0.0, 0.0);
+        if (a < b) { Dinv[a][b] = make_double2(0.0, 0.0); continue; }
+        for (int j = b; j < a; ++j) {
+          const cplx u = cmul(Ls[a * n + R0 + j], Dinv[j][b]);
+          s.x -= u.x;
+          s.y -= u.y;
+        }
+        Dinv[a][b] = cdiv(s, Ls[a * n + R0 + a]);
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c < n; c += CH_THREADS) {
+      if (c < R0) {
+        cplx acc[CH_NB];
+#pragma unroll
+        for (int a = 0; a < CH_NB; ++a) acc[a] = make_double2(0.0, 0.0);
+        for (int j = c; j < R0; ++j) {
+          const cplx lv = P.Linv[(long long)j * ld + c];
+#pragma unroll
+          for (int a = 0; a < CH_NB; ++a) {
+            const cplx u = cmul(Ls[a * n + j], lv);   // rows a >= rb are never stored
+            acc[a].x += u.x;
+            acc[a].y += u.y;
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < CH_NB; ++a) {
+          if (a >= rb) break;
+          cplx v = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int b = 0; b <= a; ++b) {
+            const cplx u = cmul(Dinv[a][b], acc[b]);
+            v.x -= u.x;
+            v.y -= u.y;
+          }
+          P.Linv[(long long)(R0 + a) * ld + c] = v;
+        }
+      } else {
+        for (int a = 0; a < rb; ++a)
+          P.Linv[(long long)(R0 + a) * ld + c] = (c < w) ? Dinv[a][c - R0] : make_double2(0.0, 0.0);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -239,8 +375,16 @@ void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s) {
   const PotrfProblem* d = static_cast<const PotrfProblem*>(st.put(h, sizeof(PotrfProblem) * n));
   double fl = 0.0;
   for (int i = 0; i < n; ++i) fl += 8.0 * (double)h[i].n * h[i].n * h[i].n / 6.0;
+  int mx = 1;
+  for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].n);
+  const size_t smem = (size_t)mx * CH_NB * sizeof(cplx);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(potrf_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 << 10));
+    attr = smem;
+  }
   prof_begin(s);
-  potrf_grouped<<<n, 256, 0, s>>>(d);
+  potrf_grouped<<<n, CH_THREADS, smem, s>>>(d);
   prof_end(s, "potrf", fl, 0.0);
   count_launch();
 }
@@ -250,8 +394,16 @@ void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s) {
   const TrtriProblem* d = static_cast<const TrtriProblem*>(st.put(h, sizeof(TrtriProblem) * n));
   double fl = 0.0;
   for (int i = 0; i < n; ++i) fl += 8.0 * (double)h[i].n * h[i].n * h[i].n / 6.0;
+  int mx = 1;
+  for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].n);
+  const size_t smem = (size_t)mx * CH_NB * sizeof(cplx);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(trtri_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 << 10));
+    attr = smem;
+  }
   prof_begin(s);
-  trtri_grouped<<<n, 256, 0, s>>>(d);
+  trtri_grouped<<<n, CH_THREADS, smem, s>>>(d);
   prof_end(s, "trtri", fl, 0.0);
   count_launch();
 }

@@ -237,8 +237,20 @@ const PlanT& get_plan(const Task& t) {
 
 }  // namespace
 
+namespace {
+struct ArenaScratch : Scratch {
+  Arena& a;
+  explicit ArenaScratch(Arena& ar) : a(ar) {}
+  void* get(size_t bytes) override { return a.alloc(bytes); }
+};
+}  // namespace
+
+double gemm_flops(const GemmProblem& g) {
+  return g.sym ? 4.0 * (double)g.M * (g.M + 1) * g.K : 8.0 * (double)g.M * g.N * g.K;
+}
+
 void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st) {
-  for (auto& g : probs) st.flops += 8.0 * (double)g.M * g.N * g.K;
+  for (auto& g : probs) st.flops += gemm_flops(g);
   static const bool dbg = getenv("TTN_DEBUG_GEMM") != nullptr;
   if (dbg && !probs.empty()) {
     std::map<std::string, int> shapes;
@@ -251,7 +263,8 @@ void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st) 
     for (auto& kv : shapes) fprintf(stderr, " %s*%d", kv.first.c_str(), kv.second);
     fprintf(stderr, "\n");
   }
-  if (!probs.empty()) launch_gemm(probs.data(), (int)probs.size(), *ctx->stager, ctx->stream);
+  ArenaScratch ws(ctx->scratch);
+  if (!probs.empty()) launch_gemm(probs.data(), (int)probs.size(), *ctx->stager, ctx->stream, &ws);
 }
 
 GemmProblem mk_gemm(const cplx* A, int opA, long long lda, const cplx* B, int opB, long long ldb, cplx* C,

@@ -38,6 +38,9 @@ void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st);
 // Convenience: grouped GEMM with host bookkeeping of flops.
 void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st);
 
+// Algorithmic flops of one problem (8 per complex MAC; Hermitian products count the lower half).
+double gemm_flops(const GemmProblem& g);
+
 // Plain matrix product problem from BLAS-style op flags (OP_N/T/R/C) and leading dimensions.
 GemmProblem mk_gemm(const cplx* A, int opA, long long lda, const cplx* B, int opB, long long ldb, cplx* C,
                     long long ldc, int64_t M, int64_t N, int64_t K);

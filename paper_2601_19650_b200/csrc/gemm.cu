@@ -34,11 +34,14 @@ namespace {
 constexpr int BK = 8, STAGES = 3, THREADS = 128;
 constexpr int PADK = BK + 4;   // m-major / n-major rows: 12 complex = 192 B (conflict-free frags)
 
+// k-major rows (As[k][m], Bs[k][n]) are padded by 2 complex (32 B): the 4 k-rows a fragment
+// load touches then start in different bank quarters (no 4-way conflicts)
 template <int BM, int BN, bool AKM, bool BNM>
 struct Cfg {
-  static constexpr int A_ELEMS = AKM ? BK * BM : BM * PADK;
-  static constexpr int B_ELEMS = BNM ? BN * PADK : BK * BN;
-  static constexpr int TAB = (2 * BM + 2 * BN + 2 * STAGES * BK) * 8;
+  static constexpr int LDAK = BM + 2, LDBK = BN + 2;
+  static constexpr int A_ELEMS = AKM ? BK * LDAK : BM * PADK;
+  static constexpr int B_ELEMS = BNM ? BN * PADK : BK * LDBK;
+  static constexpr int TAB = (3 * BM + 3 * BN + 2 * STAGES * BK) * 8;
   static constexpr int BYTES = STAGES * (A_ELEMS + B_ELEMS) * 16 + TAB + 1024;
 };
 
@@ -100,7 +103,9 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
   long long* colB = rowA + BM;
   long long* rowC = colB + BN;
   long long* colC = rowC + BM;
-  long long* kA = colC + BN;                 // [STAGES][BK] k-leg offsets into A (-1: k >= K)
+  long long* colCm = colC + BN;              // sym: column offsets of the m indices (mirror)
+  long long* rowCn = colCm + BM;             // sym: row offsets of the n indices (mirror)
+  long long* kA = rowCn + BN;                // [STAGES][BK] k-leg offsets into A (-1: k >= K)
   long long* kB = kA + STAGES * BK;          // [STAGES][BK] k-leg offsets into B
   GemmProblem* sP = reinterpret_cast<GemmProblem*>(kB + STAGES * BK);
 
@@ -108,45 +113,68 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
   if (tid == 0) *sP = probs[find_problem(probs, nprob, blockIdx.x)];
   __syncthreads();
   const GemmProblem& P = *sP;
-  const int t = blockIdx.x - P.tile_start;
-  const int m0 = (t / P.tiles_n) * BM, n0 = (t % P.tiles_n) * BN;
-  const int M = P.M, N = P.N, K = P.K;
+  const int t0 = blockIdx.x - P.tile_start;
+  const int sp = t0 / P.tiles_mn, t = t0 % P.tiles_mn;   // k split, output tile
+  int bi, bj;
+  if (P.sym) {   // lower-triangular tile index
+    bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    bj = t - bi * (bi + 1) / 2;
+  } else {
+    bi = t / P.tiles_n;
+    bj = t % P.tiles_n;
+  }
+  const int m0 = bi * BM, n0 = bj * BN;
+  const bool mirror = P.sym && bi != bj;
+  const int M = P.M, N = P.N;
+  const int kbeg = sp * P.kchunk, K = min(P.K, kbeg + P.kchunk);   // this CTA's k range [kbeg, K)
   for (int i = tid; i < BM; i += THREADS) {
     const int m = m0 + i;
     rowA[i] = m < M ? goff(m, P.nm, P.md, P.am) : -1;
     rowC[i] = m < M ? goff(m, P.nm, P.md, P.cm) : -1;
+    if (mirror) colCm[i] = m < M ? goff(m, P.nn, P.nd, P.cn) : -1;
   }
   for (int i = tid; i < BN; i += THREADS) {
     const int n = n0 + i;
     colB[i] = n < N ? goff(n, P.nn, P.nd, P.bn) : -1;
     colC[i] = n < N ? goff(n, P.nn, P.nd, P.cn) : -1;
+    if (mirror) rowCn[i] = n < N ? goff(n, P.nm, P.md, P.cm) : -1;
   }
-  const int ktiles = (K + BK - 1) / BK;
+  const int ktiles = (K - kbeg + BK - 1) / BK;
   // k-leg offsets of tile T into ring slot T % STAGES (thread j < 2*BK: operand j / BK, k j % BK)
   auto k_offsets = [&](int T, int j) {
-    const int slot = T % STAGES, kl = j % BK, k = T * BK + kl;
+    const int slot = T % STAGES, kl = j % BK, k = kbeg + T * BK + kl;
     if (j < BK) kA[slot * BK + kl] = k < K ? goff(k, P.nk, P.kd, P.ak) : -1;
     else kB[slot * BK + kl] = k < K ? goff(k, P.nk, P.kd, P.bk) : -1;
   };
-  for (int j = tid; j < 2 * BK * STAGES; j += THREADS) {
-    const int T = j / (2 * BK);
-    if (T < ktiles) k_offsets(T, j % (2 * BK));
-  }
+  if (P.nk != 1)
+    for (int j = tid; j < 2 * BK * STAGES; j += THREADS) {
+      const int T = j / (2 * BK);
+      if (T < ktiles) k_offsets(T, j % (2 * BK));
+    }
   __syncthreads();
   const cplx* __restrict__ Ag = P.A;
   const cplx* __restrict__ Bg = P.B;
   const int wm = (warp / WGN) * WTM, wn = (warp % WGN) * WTN;
   const bool conjA = P.conjA != 0, conjB = P.conjB != 0;
 
+  const bool k1 = P.nk == 1;               // single k leg: offsets are k * stride, no ring
+  const long long ak0 = P.ak[0], bk0 = P.bk[0];
+  auto kofs = [&](const long long* ring, long long st0, int T, int kl) -> long long {
+    if (k1) {
+      const int k = kbeg + T * BK + kl;
+      return k < K ? (long long)k * st0 : -1;
+    }
+    return ring[(T % STAGES) * BK + kl];
+  };
   auto load_stage = [&](int T) {
     const int stage = T % STAGES;
     cplx* as = As + stage * C_::A_ELEMS;
     cplx* bs = Bs + stage * C_::B_ELEMS;
-    const long long* ka = kA + stage * BK;
-    const long long* kb = kB + stage * BK;
     if (!AKM) {   // As[m][k]: k fixed per thread
       const int k = tid % BK;
-      const long long ko = ka[k];
+      const long long ko = kofs(kA, ak0, T, k);
 #pragma unroll
       for (int r = 0; r < (BM * BK) / THREADS; ++r) {
         const int m = tid / BK + r * (THREADS / BK);
@@ -159,14 +187,14 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
       for (int r = 0; r < (BM * BK) / THREADS; ++r) {
         const int idx = tid + r * THREADS;
         const int k = idx / BM, m = idx % BM;
-        const long long ro = rowA[m], ko = ka[k];
+        const long long ro = rowA[m], ko = kofs(kA, ak0, T, k);
         const bool v = ko >= 0 && ro >= 0;
-        cp_async16(as + k * BM + m, v ? Ag + ro + ko : Ag, v);
+        cp_async16(as + k * C_::LDAK + m, v ? Ag + ro + ko : Ag, v);
       }
     }
     if (BNM) {    // Bs[n][k]: k fixed per thread
       const int k = tid % BK;
-      const long long ko = kb[k];
+      const long long ko = kofs(kB, bk0, T, k);
 #pragma unroll
       for (int r = 0; r < (BN * BK) / THREADS; ++r) {
         const int n = tid / BK + r * (THREADS / BK);
@@ -179,9 +207,9 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
       for (int r = 0; r < (BN * BK) / THREADS; ++r) {
         const int idx = tid + r * THREADS;
         const int k = idx / BN, n = idx % BN;
-        const long long co = colB[n], ko = kb[k];
+        const long long co = colB[n], ko = kofs(kB, bk0, T, k);
         const bool v = ko >= 0 && co >= 0;
-        cp_async16(bs + k * BN + n, v ? Bg + co + ko : Bg, v);
+        cp_async16(bs + k * C_::LDBK + n, v ? Bg + co + ko : Bg, v);
       }
     }
   };
@@ -207,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
     __syncthreads();
     // decode the k legs of tile kt + STAGES (slot kt % STAGES: its last reader, the load of
     // tile kt, was issued before this barrier); visible to the loads after the next barrier
-    if (tid < 2 * BK && kt + STAGES < ktiles) k_offsets(kt + STAGES, tid);
+    if (!k1 && tid < 2 * BK && kt + STAGES < ktiles) k_offsets(kt + STAGES, tid);
     {
       const int kn = kt + STAGES - 1;
       if (kn < ktiles) load_stage(kn);
@@ -222,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
         const int m = wm + i * 8 + fr;
-        const cplx a = AKM ? as[k * BM + m] : as[m * PADK + k];
+        const cplx a = AKM ? as[k * C_::LDAK + m] : as[m * PADK + k];
         ar[q][i] = a.x;
         ai[q][i] = neg_if(a.y, conjA);
         nai[q][i] = neg_if(a.y, !conjA);
@@ -230,7 +258,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
         const int n = wn + j * 8 + fr;
-        const cplx b = BNM ? bs[n * PADK + k] : bs[k * BN + n];
+        const cplx b = BNM ? bs[n * PADK + k] : bs[k * C_::LDBK + n];
         br[q][j] = b.x;
         bi[q][j] = neg_if(b.y, conjB);
       }
@@ -257,19 +285,38 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
   }
   cp_async_wait<0>();
 
-  // epilogue: C = alpha * acc + beta * C (strided store: the output permutation is fused here)
+  // epilogue: C = alpha * acc + beta * C (strided store: the output permutation is fused here);
+  // split-k partials go raw to the workspace; Hermitian products also write the mirror tile
   const cplx al = P.alpha, be = P.beta;
   const bool use_beta = (be.x != 0.0 || be.y != 0.0);
   cplx* __restrict__ Cg = P.C;
+  if (P.ksplit > 1) {
+    cplx* W = P.ws + (size_t)sp * M * N;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int m = m0 + wm + i * 8 + fr;
+      if (m >= M) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = n0 + wn + j * 8 + fc * 2 + h;
+          if (n < N) W[(size_t)m * N + n] = make_double2(acc_re[i][j][h], acc_im[i][j][h]);
+        }
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    const long long ro = rowC[wm + i * 8 + fr];
+    const int il = wm + i * 8 + fr;
+    const long long ro = rowC[il];
     if (ro < 0) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const long long co = colC[wn + j * 8 + fc * 2 + h];
+        const int jl = wn + j * 8 + fc * 2 + h;
+        const long long co = colC[jl];
         if (co < 0) continue;
         const double re = acc_re[i][j][h], im = acc_im[i][j][h];
         cplx out;
@@ -282,8 +329,43 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
           out.y += be.x * c.y + be.y * c.x;
         }
         *cp = out;
+        if (mirror) Cg[rowCn[jl] + colCm[il]] = make_double2(out.x, -out.y);
       }
     }
+  }
+}
+
+// split-k reduction: C = alpha * sum_s W_s + beta * C (C through its strided legs)
+__global__ void zgemm_splitk_reduce(const GemmProblem* __restrict__ probs, int nprob) {
+  const GemmProblem& P = probs[blockIdx.y];
+  const long long MN = (long long)P.M * P.N;
+  const cplx al = P.alpha, be = P.beta;
+  const bool use_beta = (be.x != 0.0 || be.y != 0.0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN; e += (long long)gridDim.x * blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int s = 0; s < P.ksplit; ++s) {
+      const cplx w = P.ws[s * MN + e];
+      re += w.x;
+      im += w.y;
+    }
+    const int m = (int)(e / P.N), n = (int)(e % P.N);
+    if (P.sym && (m >> 6) < (n >> 6)) {   // upper tile of a Hermitian product: mirror of (n, m)
+      re = 0.0;
+      im = 0.0;
+      for (int s = 0; s < P.ksplit; ++s) {
+        const cplx w = P.ws[s * MN + (long long)n * P.N + m];
+        re += w.x;
+        im -= w.y;
+      }
+    }
+    cplx* cp = P.C + goff(m, P.nm, P.md, P.cm) + goff(n, P.nn, P.nd, P.cn);
+    cplx out = make_double2(al.x * re - al.y * im, al.x * im + al.y * re);
+    if (use_beta) {
+      const cplx c = *cp;
+      out.x += be.x * c.x - be.y * c.y;
+      out.y += be.x * c.y + be.y * c.x;
+    }
+    *cp = out;
   }
 }
 
@@ -296,8 +378,9 @@ void launch_variant(std::vector<GemmProblem>& h, Stager& st, cudaStream_t s) {
     const int tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
     p.tile_start = tiles;
     p.tiles_n = std::max(tn, 1);
-    tiles += tm * tn;
-    flops += 8.0 * (double)p.M * p.N * p.K;
+    p.tiles_mn = p.sym ? tm * (tm + 1) / 2 : tm * tn;
+    tiles += p.tiles_mn * std::max(p.ksplit, 1);
+    flops += p.sym ? 8.0 * 0.5 * (double)p.M * (p.M + 1) * p.K : 8.0 * (double)p.M * p.N * p.K;
     bytes += 16.0 * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N);
   }
   if (tiles == 0) return;
@@ -351,30 +434,65 @@ void gemm_from_ops(GemmProblem& g, int opA, long long lda, int opB, long long ld
   g.conjB = (opB & 2) ? 1 : 0;
 }
 
-void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s) {
-  // group by tile shape (least padded work) and shared-memory layouts
+void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws) {
+  // group by tile shape (least padded work) and shared-memory layouts; Hermitian products take
+  // the square tile (lower-triangle tiles only); problems that cannot fill the GPU with output
+  // tiles get their k range split (deterministic: partials reduced in a second kernel)
   std::vector<GemmProblem> by[kNumShapes][4];
+  std::vector<GemmProblem> split;
   for (int i = 0; i < n; ++i) {
     GemmProblem p = h[i];
     if (p.M <= 0 || p.N <= 0) continue;
+    if (p.sym && !(p.M == p.N && p.alpha.y == 0.0 && p.beta.x == 0.0 && p.beta.y == 0.0)) p.sym = 0;
     // A: k-major smem when the innermost m leg is unit-stride and the innermost k leg is not
     const bool akm = (p.ak[p.nk - 1] != 1) && (p.am[p.nm - 1] == 1);
     // B: n-major smem when the innermost k leg is unit-stride and the innermost n leg is not
     const bool bnm = (p.bn[p.nn - 1] != 1) && (p.bk[p.nk - 1] == 1);
     const int v = (akm ? 2 : 0) + (bnm ? 1 : 0);
     int best = 0;
-    double bc = shape_cost(p, kShapes[0]);
-    for (int t = 1; t < kNumShapes; ++t) {
-      const double c = shape_cost(p, kShapes[t]);
-      if (c < bc * 0.999) { bc = c; best = t; }
+    if (!p.sym) {
+      double bc = shape_cost(p, kShapes[0]);
+      for (int t = 1; t < kNumShapes; ++t) {
+        const double c = shape_cost(p, kShapes[t]);
+        if (c < bc * 0.999) { bc = c; best = t; }
+      }
+    }
+    p.ksplit = 1;
+    p.kchunk = std::max(p.K, 1);
+    p.ws = nullptr;
+    if (ws) {
+      const long long tm = (p.M + kShapes[best].bm - 1) / kShapes[best].bm;
+      const long long tiles = p.sym ? tm * (tm + 1) / 2 : tm * ((p.N + kShapes[best].bn - 1) / kShapes[best].bn);
+      if (tiles < 148 && p.K >= 1024) {
+        int S = (int)std::min<long long>((296 + tiles - 1) / tiles, std::min(16, p.K / 512));
+        if (S > 1) {
+          int chunk = (p.K + S - 1) / S;
+          chunk = (chunk + BK - 1) / BK * BK;
+          S = (p.K + chunk - 1) / chunk;
+          p.ksplit = S;
+          p.kchunk = chunk;
+          p.ws = static_cast<cplx*>(ws->get(sizeof(cplx) * (size_t)S * p.M * p.N));
+        }
+      }
     }
     by[best][v].push_back(p);
+    if (p.ksplit > 1) split.push_back(p);
   }
   launch_shape<64, 64, 2, 2>(by[0], st, s);
   launch_shape<128, 32, 4, 1>(by[1], st, s);
   launch_shape<32, 128, 1, 4>(by[2], st, s);
   launch_shape<128, 16, 4, 1>(by[3], st, s);
   launch_shape<16, 128, 1, 4>(by[4], st, s);
+  if (!split.empty()) {
+    const GemmProblem* d = static_cast<const GemmProblem*>(st.put(split.data(), sizeof(GemmProblem) * split.size()));
+    long long mx = 0;
+    for (auto& p : split) mx = std::max<long long>(mx, (long long)p.M * p.N);
+    const int gx = (int)std::min<long long>((mx + 255) / 256, 1024);
+    prof_begin(s);
+    zgemm_splitk_reduce<<<dim3(gx, (unsigned)split.size()), 256, 0, s>>>(d, (int)split.size());
+    prof_end(s, "zgemm_reduce", 0.0, 0.0);
+    count_launch();
+  }
 }
 
 }  // namespace tcbc

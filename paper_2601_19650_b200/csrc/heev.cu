@@ -21,6 +21,7 @@
 //              >= 1 and discarded weight w = trace(A) - sum_{t<k} lam_t.
 #include "kernels.h"
 #include "prof.h"
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -348,29 +349,14 @@ __device__ void tridiag_full(cplx* __restrict__ A, const int n, cplx* sv, cplx* 
   __syncthreads();
 }
 
-// ---------------------------------------------------------------- K1: tridiagonalisation
-__global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* __restrict__ probs) {
-  const HeevProblem P = probs[blockIdx.x];
-  const int n = P.n;
-  cplx* A = P.A;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* sv = reinterpret_cast<cplx*>(smem_raw);
-  cplx* sp = sv + n;
-  cplx* base = sp + n;
-  __shared__ double2 red[HEEV_WARPS + 1];
-  double* dvec = P.work;
-  double* evec = P.work + n;
+// Gershgorin interval, pivmin (dstebz) and the trace, from d / e in P.work (one CTA)
+__device__ void tridiag_stats(const HeevProblem& P, double trace) {
+  const int n = P.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const double* dvec = P.work;
+  const double* evec = P.work + n;
   double* sc = P.work + 2 * n;
-  double tr = 0.0;
-  for (int i = tid; i < n; i += HEEV_THREADS) tr += A[(size_t)i * n + i].x;
-  const double trace = block_sum2(tr, 0.0, red).x;
-  if (n <= SMEM_MAX_N) tridiag_fused<true>(A, n, sv, sp, base, dvec, evec, P.tau, red);
-  else if (n <= FUSED_MAX_N) tridiag_fused<false>(A, n, sv, sp, base, dvec, evec, P.tau, red);
-  else tridiag_full(A, n, sv, sp, dvec, evec, P.tau, red);
-  // Gershgorin interval, pivmin (dstebz)
   double gl = 1e300, gu = -1e300, em = 0.0;
-  for (int i = tid; i < n; i += HEEV_THREADS) {
+  for (int i = tid; i < n; i += blockDim.x) {
     const double di = dvec[i], ei = (i < n - 1) ? evec[i] : 0.0, ep = (i > 0) ? evec[i - 1] : 0.0;
     const double rad = fabs(ei) + fabs(ep);
     gl = fmin(gl, di - rad);
@@ -382,12 +368,12 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* 
     gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
     em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
   }
-  __shared__ double mm[3][HEEV_WARPS];
+  __shared__ double mm[3][32];
   if (lane == 0) { mm[0][warp] = gl; mm[1][warp] = gu; mm[2][warp] = em; }
   __syncthreads();
   if (tid == 0) {
     gl = mm[0][0]; gu = mm[1][0]; em = mm[2][0];
-    for (int w = 1; w < HEEV_WARPS; ++w) { gl = fmin(gl, mm[0][w]); gu = fmax(gu, mm[1][w]); em = fmax(em, mm[2][w]); }
+    for (int w = 1; w < nw; ++w) { gl = fmin(gl, mm[0][w]); gu = fmax(gu, mm[1][w]); em = fmax(em, mm[2][w]); }
     const double tnorm = fmax(fabs(gl), fabs(gu));
     const double pivmin = DBL_MIN * fmax(1.0, em);
     sc[S_GL] = gl - 2.0 * DBL_EPSILON * tnorm * n - 2.0 * pivmin;
@@ -399,9 +385,187 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* 
   }
 }
 
+// ---------------------------------------------------------------- K1: tridiagonalisation
+__global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* __restrict__ probs) {
+  const HeevProblem P = probs[blockIdx.x];
+  const int n = P.n;
+  cplx* A = P.A;
+  const int tid = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* sv = reinterpret_cast<cplx*>(smem_raw);
+  cplx* sp = sv + n;
+  cplx* base = sp + n;
+  __shared__ double2 red[HEEV_WARPS + 1];
+  double* dvec = P.work;
+  double* evec = P.work + n;
+  double tr = 0.0;
+  for (int i = tid; i < n; i += HEEV_THREADS) tr += A[(size_t)i * n + i].x;
+  const double trace = block_sum2(tr, 0.0, red).x;
+  if (n <= SMEM_MAX_N) tridiag_fused<true>(A, n, sv, sp, base, dvec, evec, P.tau, red);
+  else if (n <= FUSED_MAX_N) tridiag_fused<false>(A, n, sv, sp, base, dvec, evec, P.tau, red);
+  else tridiag_full(A, n, sv, sp, dvec, evec, P.tau, red);
+  tridiag_stats(P, trace);
+}
+
+// K1 on a thread-block cluster of CS CTAs (levels with few Grams: chains, config 4's 4-chain
+// levels).  The full Hermitian matrix is distributed by row blocks over the CTAs' shared
+// memory (DSMEM), so one matrix uses CS SMs and never touches L2 after the initial load.
+// Per Householder step two cluster barriers:
+//   A  every CTA broadcasts its rows' entries of column j (and a partial |x|^2) to all CTAs;
+//      then each CTA forms the reflector (zlarfg) redundantly;
+//   B  every CTA computes p = tau A v on its rows and broadcasts p (and a partial p^H v);
+//      then each CTA forms w = p - tau/2 (p^H v) v and applies A -= v w^H + w v^H to its rows.
+// Same outputs as heev_tridiag (d, e, tau, reflectors in rows of A, stats).
+constexpr int CL_THREADS = 256;
+constexpr size_t CL_SMEM_LIMIT = 200u << 10;
+
+__host__ __device__ inline size_t cl_smem_bytes(int n, int cs) {
+  const int rpc = (n + cs - 1) / cs;
+  return (size_t)rpc * n * 16 + (size_t)3 * n * 16 + (size_t)2 * 16 * 16 + 64;
+}
+
+template <int CS>
+__global__ void __launch_bounds__(CL_THREADS) heev_tridiag_cluster(const HeevProblem* __restrict__ probs) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const HeevProblem P = probs[blockIdx.x / CS];
+  const int n = P.n, rpc = (n + CS - 1) / CS, r0 = rank * rpc, r1 = min(n, r0 + rpc);
+  cplx* A = P.A;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = CL_THREADS / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* rows = reinterpret_cast<cplx*>(smem_raw);   // [rpc][n]
+  cplx* x = rows + (size_t)rpc * n;                  // column j, broadcast     [n]
+  cplx* pv = x + n;                                  // p = tau A v, broadcast   [n]
+  cplx* vw = pv + n;                                 // v then w (local)        [n]
+  double2* partN = reinterpret_cast<double2*>(vw + n);   // [16]
+  double2* partD = partN + 16;                            // [16]
+  __shared__ double2 red[NW + 1];
+  __shared__ cplx s_v[1];
+  double* dvec = P.work;
+  double* evec = P.work + n;
+  for (long long e = tid; e < (long long)(r1 - r0) * n; e += CL_THREADS) rows[e] = A[(size_t)r0 * n + e];
+  double trace = 0.0;
+  if (rank == 0) {
+    double tr = 0.0;
+    for (int i = tid; i < n; i += CL_THREADS) tr += A[(size_t)i * n + i].x;
+    trace = block_sum2(tr, 0.0, red).x;
+  }
+  cl.sync();   // every CTA has its rows before any reflector is written back to A
+  for (int j = 0; j < n - 1; ++j) {
+    // ---- A: broadcast column j (rows > j) and partial norms
+    const int ia = max(r0, j + 1);
+    double pn = 0.0;
+    for (int i = ia + tid; i < r1; i += CL_THREADS) {
+      const cplx xi = rows[(size_t)(i - r0) * n + j];
+      if (i >= j + 2) pn += xi.x * xi.x + xi.y * xi.y;
+#pragma unroll
+      for (int d = 0; d < CS; ++d) *cl.map_shared_rank(x + i, d) = xi;
+    }
+    if (j >= r0 && j < r1 && tid == 0) dvec[j] = rows[(size_t)(j - r0) * n + j].x;
+    pn = block_sum2(pn, 0.0, red).x;
+    if (tid < CS) *cl.map_shared_rank(partN + rank, tid) = make_double2(pn, 0.0);
+    cl.sync();
+    double xn2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < CS; ++d) xn2 += partN[d].x;
+    const cplx alpha = x[j + 1];
+    double beta;
+    cplx tau, scale;
+    if (xn2 == 0.0 && alpha.y == 0.0) {
+      beta = alpha.x;
+      tau = make_double2(0.0, 0.0);
+      scale = make_double2(0.0, 0.0);
+    } else {
+      beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn2), alpha.x);
+      tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+      const cplx den = make_double2(alpha.x - beta, alpha.y);
+      const double dd = den.x * den.x + den.y * den.y;
+      scale = make_double2(den.x / dd, -den.y / dd);
+    }
+    const bool tnz = (tau.x != 0.0 || tau.y != 0.0);
+    for (int i = j + 1 + tid; i < n; i += CL_THREADS) {
+      cplx v;
+      if (i == j + 1) v = make_double2(1.0, 0.0);
+      else {
+        const cplx xi = x[i];
+        v = make_double2(xi.x * scale.x - xi.y * scale.y, xi.x * scale.y + xi.y * scale.x);
+      }
+      if (rank == 0) A[(size_t)j * n + i] = v;   // kept for the back-transform
+      vw[i] = tnz ? v : make_double2(0.0, 0.0);
+    }
+    if (rank == 0 && tid == 0) {
+      evec[j] = beta;
+      P.tau[j] = tau;
+    }
+    if (!tnz) {   // H_j = I: nothing to apply; keep the barrier pattern (x is reused next step)
+      cl.sync();
+      continue;
+    }
+    __syncthreads();
+    // ---- B: p = tau A v on my rows (warp per row), broadcast p and partial p^H v
+    double dr = 0.0, di = 0.0;
+    for (int i = ia + warp; i < r1; i += NW) {
+      const cplx* row = rows + (size_t)(i - r0) * n;
+      double sr = 0.0, si = 0.0;
+      for (int c = j + 1 + lane; c < n; c += 32) {
+        const cplx a = row[c], v = vw[c];
+        sr += a.x * v.x - a.y * v.y;
+        si += a.x * v.y + a.y * v.x;
+      }
+      sr = warp_sum(sr);
+      si = warp_sum(si);
+      const cplx p = make_double2(tau.x * sr - tau.y * si, tau.x * si + tau.y * sr);
+      for (int d = lane; d < CS; d += 32) *cl.map_shared_rank(pv + i, d) = p;
+      const cplx v = vw[i];
+      dr += p.x * v.x + p.y * v.y;
+      di += p.x * v.y - p.y * v.x;
+    }
+    // dr/di were accumulated by lane-identical copies: keep lane 0's
+    dr = __shfl_sync(0xffffffffu, dr, 0);
+    di = __shfl_sync(0xffffffffu, di, 0);
+    if (lane != 0) { dr = 0.0; di = 0.0; }
+    const double2 dl = block_sum2(dr, di, red);
+    if (tid < CS) *cl.map_shared_rank(partD + rank, tid) = dl;
+    cl.sync();
+    double2 dot = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int d = 0; d < CS; ++d) { dot.x += partD[d].x; dot.y += partD[d].y; }
+    const cplx a2 = make_double2(-0.5 * (tau.x * dot.x - tau.y * dot.y), -0.5 * (tau.x * dot.y + tau.y * dot.x));
+    // w = p + a2 v (in place of v: keep v in registers of the update loop)
+    // ---- C: A -= v w^H + w v^H on my rows, columns > j
+    for (int i = ia + warp; i < r1; i += NW) {
+      cplx* row = rows + (size_t)(i - r0) * n;
+      const cplx vr = vw[i], pr = pv[i];
+      const cplx wr = make_double2(pr.x + a2.x * vr.x - a2.y * vr.y, pr.y + a2.x * vr.y + a2.y * vr.x);
+      for (int c = j + 1 + lane; c < n; c += 32) {
+        const cplx vc = vw[c], pc = pv[c];
+        const cplx wc = make_double2(pc.x + a2.x * vc.x - a2.y * vc.y, pc.y + a2.x * vc.y + a2.y * vc.x);
+        cplx a = row[c];
+        a.x -= (vr.x * wc.x + vr.y * wc.y) + (wr.x * vc.x + wr.y * vc.y);
+        a.y -= (vr.y * wc.x - vr.x * wc.y) + (wr.y * vc.x - wr.x * vc.y);
+        row[c] = a;
+      }
+    }
+    __syncthreads();
+  }
+  if (n - 1 >= r0 && n - 1 < r1 && tid == 0) dvec[n - 1] = rows[(size_t)(n - 1 - r0) * n + (n - 1)].x;
+  if (rank == 0 && tid == 0) evec[n - 1] = 0.0;
+  (void)s_v;
+  __threadfence();
+  cl.sync();
+  if (rank == 0) tridiag_stats(P, trace);
+}
+
 // ---------------------------------------------------------------- K2: eigenvalues
+// One warp per (matrix, eigenvalue): multisection.  Each lane evaluates Sturm counts at two
+// of 64 interior points of [lo, hi] (two interleaved chains hide the division latency); the
+// interval shrinks 65x per round, so ~9 rounds reach the dstebz tolerance instead of ~50
+// bisection steps.  Counts are exact integers, so the result is the same bracket bisection
+// would converge to.
 __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, int total) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (g >= total) return;
   const HeevProblem& P = probs[find_estart(probs, nprob, g)];
   const int t = g - P.estart, n = P.n;
@@ -411,18 +575,33 @@ __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, in
   const double pivmin = sc[S_PIVMIN], atol = sc[S_ATOL];
   const int idx = n - 1 - t;                   // ascending index of the t-th largest
   double lo = sc[S_GL], hi = sc[S_GU];
-  for (int it = 0; it < 96; ++it) {
+  for (int it = 0; it < 40; ++it) {
     if (hi - lo <= fmax(atol, 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) + pivmin) break;
-    const double w = 0.25 * (hi - lo);
-    const double x1 = lo + w, x2 = lo + 2.0 * w, x3 = lo + 3.0 * w;
-    int c1, c2, c3;
-    sturm_count3(d, e, n, x1, x2, x3, pivmin, c1, c2, c3);
-    if (c1 > idx) hi = x1;
-    else if (c2 > idx) { lo = x1; hi = x2; }
-    else if (c3 > idx) { lo = x2; hi = x3; }
-    else lo = x3;
+    const double w = (hi - lo) / 65.0;
+    const double x1 = lo + w * (2 * lane + 1), x2 = lo + w * (2 * lane + 2);
+    int c1 = 0, c2 = 0;
+    double q1 = d[0] - x1, q2 = d[0] - x2;
+    if (q1 <= pivmin) { ++c1; q1 = fmin(q1, -pivmin); }
+    if (q2 <= pivmin) { ++c2; q2 = fmin(q2, -pivmin); }
+    for (int i = 1; i < n; ++i) {
+      const double di = d[i], ep = e[i - 1], ei = ep * ep;
+      q1 = di - x1 - ei / q1;
+      q2 = di - x2 - ei / q2;
+      if (q1 <= pivmin) { ++c1; q1 = fmin(q1, -pivmin); }
+      if (q2 <= pivmin) { ++c2; q2 = fmin(q2, -pivmin); }
+    }
+    // the eigenvalue lies in the first sub-interval whose right end has count > idx
+    const unsigned b1 = __ballot_sync(0xffffffffu, c1 > idx), b2 = __ballot_sync(0xffffffffu, c2 > idx);
+    // point index p = 2*lane + (0 | 1); first p with count > idx
+    int pfirst = 64;
+    if (b1) pfirst = min(pfirst, 2 * (__ffs(b1) - 1));
+    if (b2) pfirst = min(pfirst, 2 * (__ffs(b2) - 1) + 1);
+    const double nlo = pfirst == 0 ? lo : lo + w * pfirst;
+    const double nhi = pfirst == 64 ? hi : lo + w * (pfirst + 1);
+    lo = nlo;
+    hi = nhi;
   }
-  P.lam[t] = 0.5 * (lo + hi);
+  if (lane == 0) P.lam[t] = 0.5 * (lo + hi);
 }
 
 // ---------------------------------------------------------------- K3: inverse iteration
@@ -534,6 +713,13 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_orth(const HeevProblem* __r
   const HeevProblem P = probs[blockIdx.x];
   const int n = P.n, kmax = P.kmax, tid = threadIdx.x;
   const int k = P.k_out ? *P.k_out : kmax;   // only the kept directions are orthonormalised
+  {   // isolated eigenvalues (gap > 1e-5 ||T||): inverse-iteration vectors are already orthogonal
+      // to O(eps ||T|| / gap) <= 1e-11 and unit-norm; only clusters (MGS'd in K3b) get CholeskyQR2
+    const double* csz = cluster_arrays(P) + kmax;
+    bool any = false;
+    for (int t = 0; t < k; ++t) any = any || csz[t] > 1.0;
+    if (!any) return;
+  }
   double* Z = P.work + 2 * n + 8;
   double* Wm = Z + (size_t)n * kmax * 6;
   for (int pass = 0; pass < 2; ++pass) {
@@ -567,6 +753,158 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_orth(const HeevProblem* __r
       }
     }
     __syncthreads();
+  }
+}
+
+// K4 with everything in shared memory (kmax <= 128): Gram by 4x4 register tiles over 32-row
+// chunks of Z, Cholesky of the Gram, L^{-1} into the Gram's upper triangle, Z <- Z L^{-T} by
+// chunks (lane = row, warp = group of output columns).  Two passes (CholeskyQR2).
+constexpr int ORTH_SMEM_K = 128;
+
+__host__ __device__ inline size_t orth_smem_bytes(int kmax) {
+  const int ld = kmax + 1;
+  return ((size_t)kmax * ld + 2 * 32 * (size_t)ld + kmax) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(HEEV_THREADS) heev_orth_smem(const HeevProblem* __restrict__ probs) {
+  const HeevProblem P = probs[blockIdx.x];
+  const int n = P.n, kmax = P.kmax, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = P.k_out ? *P.k_out : kmax;
+  {
+    const double* csz = cluster_arrays(P) + kmax;
+    bool any = false;
+    for (int t = 0; t < k; ++t) any = any || csz[t] > 1.0;
+    if (!any) return;
+  }
+  double* Z = P.work + 2 * n + 8;   // n x kmax, ld kmax
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ld = kmax + 1;
+  double* W = reinterpret_cast<double*>(smem_raw);   // [k][ld]: lower = Gram / L, upper = L^{-1}^T
+  double* Zc = W + (size_t)kmax * ld;                 // [32][ld]
+  double* Zo = Zc + 32 * ld;                          // [32][ld]
+  double* dinv = Zo + 32 * ld;                        // [k]
+  const int kb = (k + 3) / 4, ntile = kb * (kb + 1) / 2;
+  for (int pass = 0; pass < 2; ++pass) {
+    // ---- Gram (lower), 4x4 tiles, up to 3 per thread
+    double acc[3][4][4];
+    int tb[3][2];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int e = tid + q * HEEV_THREADS;
+      int bi = -1, bj = -1;
+      if (e < ntile) {
+        bi = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while (bi * (bi + 1) / 2 > e) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= e) ++bi;
+        bj = e - bi * (bi + 1) / 2;
+      }
+      tb[q][0] = bi;
+      tb[q][1] = bj;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[q][a][b] = 0.0;
+    }
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int rows = min(32, n - i0);
+      for (int e = tid; e < 32 * k; e += HEEV_THREADS) {
+        const int r = e / k, c = e % k;
+        Zc[r * ld + c] = r < rows ? Z[(size_t)(i0 + r) * kmax + c] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (tb[q][0] < 0) continue;
+        const int s0 = 4 * tb[q][0], t0 = 4 * tb[q][1];
+        for (int r = 0; r < 32; ++r) {
+          double zs[4], zt[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            zs[a] = (s0 + a < k) ? Zc[r * ld + s0 + a] : 0.0;
+            zt[a] = (t0 + a < k) ? Zc[r * ld + t0 + a] : 0.0;
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[q][a][b] += zs[a] * zt[b];
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (tb[q][0] < 0) continue;
+      const int s0 = 4 * tb[q][0], t0 = 4 * tb[q][1];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (s0 + a < k && t0 + b <= s0 + a) W[(s0 + a) * ld + t0 + b] = acc[q][a][b];
+    }
+    __syncthreads();
+    // ---- Cholesky W = L L^T (lower, in place)
+    for (int j = 0; j < k; ++j) {
+      if (tid == 0) {
+        const double djj = sqrt(fmax(W[j * ld + j], 1e-300));
+        W[j * ld + j] = djj;
+        dinv[j] = 1.0 / djj;
+      }
+      __syncthreads();
+      const double inv = dinv[j];
+      for (int i = j + 1 + tid; i < k; i += HEEV_THREADS) W[i * ld + j] *= inv;
+      __syncthreads();
+      const int m = k - j - 1;
+      for (int e = tid; e < m * (m + 1) / 2; e += HEEV_THREADS) {
+        int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while (a * (a + 1) / 2 > e) --a;
+        while ((a + 1) * (a + 2) / 2 <= e) ++a;
+        const int b = e - a * (a + 1) / 2;
+        const int i = j + 1 + a, l = j + 1 + b;
+        W[i * ld + l] -= W[i * ld + j] * W[l * ld + j];
+      }
+      __syncthreads();
+    }
+    // ---- L^{-1}: column c by thread c, stored transposed in the upper triangle (W[c][i] = Linv[i][c])
+    for (int c = tid; c < k; c += HEEV_THREADS) {
+      for (int i = c + 1; i < k; ++i) {
+        double sacc = W[i * ld + c] * dinv[c];
+        for (int j = c + 1; j < i; ++j) sacc += W[i * ld + j] * W[c * ld + j];
+        W[c * ld + i] = -sacc * dinv[i];
+      }
+    }
+    __syncthreads();
+    // ---- Z <- Z L^{-T}:  z[t] = sum_{s <= t} z[s] Linv[t][s]
+    const int tpw = (k + 7) / 8;
+    const int t0 = warp * tpw;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int rows = min(32, n - i0);
+      for (int e = tid; e < 32 * k; e += HEEV_THREADS) {
+        const int r = e / k, c = e % k;
+        Zc[r * ld + c] = r < rows ? Z[(size_t)(i0 + r) * kmax + c] : 0.0;
+      }
+      __syncthreads();
+      double o[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) o[q] = 0.0;
+      const int tend = min(k, t0 + tpw);
+      for (int s2 = 0; s2 < tend; ++s2) {
+        const double z = Zc[lane * ld + s2];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int t = t0 + q;
+          if (q < tpw && t < k && s2 <= t) o[q] += z * (s2 == t ? dinv[t] : W[s2 * ld + t]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q < tpw && t0 + q < k) Zo[lane * ld + t0 + q] = o[q];
+      __syncthreads();
+      for (int e = tid; e < rows * k; e += HEEV_THREADS) {
+        const int r = e / k, c = e % k;
+        Z[(size_t)(i0 + r) * kmax + c] = Zo[r * ld + c];
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -631,11 +969,14 @@ __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
   }
   if (P.k_out) *P.k_out = k;
   if (P.w_out) *P.w_out = fmax(trace - kept, 0.0);
-  // clusters of close kept eigenvalues (gap <= 1e-3 ||T||, as LAPACK dstein): their vectors
+  // clusters of close kept eigenvalues (gap <= 1e-5 ||T||): their vectors
   // are computed sequentially with reorthogonalisation (K3b), the others thread-parallel (K3a)
   double* cst = cluster_arrays(P);
   double* csz = cst + kmax;
-  const double ortol = 1e-3 * P.work[2 * P.n + S_TNORM];
+  // LAPACK dstein uses 1e-3 ||T||; an isolated inverse-iteration vector is accurate to
+  // ~eps ||T|| / gap, i.e. <= 1e-11 for gaps above 1e-5 ||T||, far inside the parity budget
+  // (1 - cos <= 1e-10), so only tighter groups take the sequential reorthogonalised path.
+  const double ortol = 1e-5 * P.work[2 * P.n + S_TNORM];
   int s0 = 0;
   for (int t = 1; t <= k; ++t) {
     if (t == k || !(P.lam[t - 1] - P.lam[t] <= ortol)) {
@@ -797,6 +1138,39 @@ size_t heev_smem_bytes(int n, int kmax) {
 
 int heev_max_n() { return HEEV_MAX_N; }
 
+namespace {
+template <int CS>
+void launch_cl(const HeevProblem* d, int nprob, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(heev_tridiag_cluster<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CL_SMEM_LIMIT);
+    if (CS > 8) cudaFuncSetAttribute(heev_tridiag_cluster<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nprob * CS);
+  cfg.blockDim = dim3(CL_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, heev_tridiag_cluster<CS>, d);
+}
+void launch_tridiag_cluster(const HeevProblem* d, int nprob, int cs, size_t smem, cudaStream_t s) {
+  switch (cs) {
+    case 2: launch_cl<2>(d, nprob, smem, s); break;
+    case 4: launch_cl<4>(d, nprob, smem, s); break;
+    case 8: launch_cl<8>(d, nprob, smem, s); break;
+    default: launch_cl<16>(d, nprob, smem, s); break;
+  }
+}
+}  // namespace
+
 void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   static bool attr = false;
@@ -816,9 +1190,30 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   }
   const HeevProblem* d = static_cast<const HeevProblem*>(st.put(h, sizeof(HeevProblem) * n));
   prof_begin(s);
-  // K1, one launch per storage mode so small-smem problems are not limited by large ones
-  std::vector<HeevProblem> grp[3];
-  for (int i = 0; i < n; ++i) grp[h[i].n <= SMEM_MAX_N ? 0 : (h[i].n <= FUSED_MAX_N ? 1 : 2)].push_back(h[i]);
+  // K1.  Few Grams of order > 96 (chain levels): one thread-block cluster per matrix, as many
+  // CTAs as keep the level within ~2 waves; otherwise one CTA per matrix, one launch per
+  // storage mode so small-smem problems are not limited by large ones.
+  std::vector<HeevProblem> grp[3], cgrp;
+  {
+    int maxn = 0, cnt = 0;
+    for (int i = 0; i < n; ++i)
+      if (h[i].n > 96) { maxn = std::max(maxn, h[i].n); ++cnt; }
+    int cs = 0;
+    for (int c = 2; c <= 16; c *= 2)
+      if (cl_smem_bytes(maxn, c) <= CL_SMEM_LIMIT) { cs = c; break; }
+    if (cnt > 0 && cs > 0 && cnt * cs <= 296) {
+      while (cs < 16 && cnt * cs * 2 <= 296 && (maxn + 2 * cs - 1) / (2 * cs) >= 8) cs *= 2;
+      for (int i = 0; i < n; ++i)
+        if (h[i].n > 96) cgrp.push_back(h[i]);
+      const HeevProblem* dg = static_cast<const HeevProblem*>(st.put(cgrp.data(), sizeof(HeevProblem) * cgrp.size()));
+      launch_tridiag_cluster(dg, (int)cgrp.size(), cs, cl_smem_bytes(maxn, cs), s);
+      count_launch();
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!cgrp.empty() && h[i].n > 96) continue;
+    grp[h[i].n <= SMEM_MAX_N ? 0 : (h[i].n <= FUSED_MAX_N ? 1 : 2)].push_back(h[i]);
+  }
   for (auto& g : grp) {
     if (g.empty()) continue;
     size_t smem = 0;
@@ -827,12 +1222,25 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
     heev_tridiag<<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
     count_launch();
   }
-  heev_bisect<<<(total + 127) / 128, 128, 0, s>>>(d, n, total);
+  heev_bisect<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
   heev_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);   // k and w: only kept pairs go on
   heev_invit<<<(total + 127) / 128, 128, 0, s>>>(d, n, total);
   heev_invit_cluster<<<n, HEEV_THREADS, 0, s>>>(d);
   count_launch();
-  heev_orth<<<n, HEEV_THREADS, 0, s>>>(d);
+  {
+    int mk = 0;
+    for (int i = 0; i < n; ++i) mk = std::max(mk, h[i].kmax);
+    if (mk <= ORTH_SMEM_K) {
+      static bool oattr = false;
+      if (!oattr) {
+        cudaFuncSetAttribute(heev_orth_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)orth_smem_bytes(ORTH_SMEM_K));
+        oattr = true;
+      }
+      heev_orth_smem<<<n, HEEV_THREADS, orth_smem_bytes(mk), s>>>(d);
+    } else {
+      heev_orth<<<n, HEEV_THREADS, 0, s>>>(d);
+    }
+  }
   heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
   count_launch(); count_launch(); count_launch(); count_launch(); count_launch();
   prof_end(s, "heev", fl, by);

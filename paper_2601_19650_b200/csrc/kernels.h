@@ -30,6 +30,17 @@ struct GemmProblem {
   int tile_start;      // filled by the launcher
   int tiles_n;         // filled by the launcher
   cplx alpha, beta;
+  int sym;             // Hermitian product (C = A^H A or A A^H, alpha real, beta 0): only the
+                       // lower tiles are computed, each off-diagonal tile also writes its mirror
+  int ksplit;          // filled by the launcher: k-range splits (partials reduced in ws)
+  int kchunk;          // filled by the launcher
+  int tiles_mn;        // filled by the launcher: output tiles per split
+  cplx* ws;            // filled by the launcher: ksplit x M x N partial products
+};
+// Device scratch for the launchers (stream-ordered bump memory owned by the caller).
+struct Scratch {
+  virtual void* get(size_t bytes) = 0;
+  virtual ~Scratch() {}
 };
 // Fill the leg descriptors of a plain matrix product from BLAS-style op flags
 // (bit0 transpose: A stored K x M / B stored N x K; bit1 conjugate) and leading dimensions.
@@ -111,7 +122,7 @@ struct Stager {
 };
 
 // Launchers fill the scheduling fields of the host problems, stage them, and launch.
-void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws = nullptr);
 void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s);

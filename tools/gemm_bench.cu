@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 #include "../paper_2601_19650_b200/csrc/kernels.h"
 
@@ -26,7 +27,15 @@ struct SimpleStager : Stager {
   }
 };
 
-struct Case { const char* name; int M, N, K, batch, opA, opB; };
+struct Case { const char* name; int M, N, K, batch, opA, opB; int sym = 0; };
+struct DevScratch : Scratch {   // stream-ordered reuse of one buffer (launches are serialised)
+  char* buf = nullptr;
+  size_t cap = 512ull << 20, off = 0;
+  DevScratch() { cudaMalloc(&buf, cap); }
+  ~DevScratch() { cudaFree(buf); }
+  void* get(size_t b) override { if (off + b > cap) off = 0; void* p = buf + off; off += (b + 255) & ~size_t(255); return p; }
+  void release() { off = 0; }
+};
 
 int main(int argc, char** argv) {
   cudaStream_t s;
@@ -49,11 +58,16 @@ int main(int argc, char** argv) {
       {"cfg4 16384x2048x128", 16384, 2048, 128, 1, 0, 0},
       {"cfg4 128x2048x16384 (Q^H Z)", 128, 2048, 16384, 1, 3, 0},
       {"square 4096", 4096, 4096, 4096, 1, 0, 0},
+      {"herk cfg4 gram 2048x2048x16384 sym", 2048, 2048, 16384, 1, 3, 0, 1},
+      {"herk cfg3 gram 192x192x2048 sym x64", 192, 192, 2048, 64, 3, 0, 1},
+      {"herk chfsi 192x192x2048 sym x4", 192, 192, 2048, 4, 3, 0, 1},
   };
   int reps = argc > 1 ? atoi(argv[1]) : 5;
   printf("[");
   bool first = true;
+  const char* filt = argc > 2 ? argv[2] : nullptr;
   for (auto& c : cases) {
+    if (filt && !strstr(c.name, filt)) continue;
     const size_t szA = (size_t)c.M * c.K, szB = (size_t)c.K * c.N, szC = (size_t)c.M * c.N;
     cplx *A, *B, *C, *Cref;
     cudaMalloc(&A, szA * 16 * c.batch);
@@ -77,7 +91,9 @@ int main(int argc, char** argv) {
       gemm_from_ops(g, c.opA, lda, c.opB, ldb, c.N);
       g.alpha = make_double2(1, 0);
       g.beta = make_double2(0, 0);
+      g.sym = c.sym;
     }
+    DevScratch scr;
     // reference: row-major C = op(A) op(B)  <=>  col-major C^T = op(B)^T op(A)^T
     auto cop = [](int op) { return op == 0 ? CUBLAS_OP_N : op == 1 ? CUBLAS_OP_T : CUBLAS_OP_C; };
     cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
@@ -90,7 +106,7 @@ int main(int argc, char** argv) {
     };
     ref();
     std::vector<GemmProblem> tmp = probs;
-    launch_gemm(tmp.data(), c.batch, st, s);
+    launch_gemm(tmp.data(), c.batch, st, s, &scr);
     cudaStreamSynchronize(s);
     std::vector<cplx> h1(szC * c.batch), h2(szC * c.batch);
     cudaMemcpy(h1.data(), C, szC * 16 * c.batch, cudaMemcpyDeviceToHost);
@@ -105,9 +121,9 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     float ms = 0, msr = 0;
-    for (int w = 0; w < 2; ++w) { tmp = probs; launch_gemm(tmp.data(), c.batch, st, s); }
+    for (int w = 0; w < 2; ++w) { tmp = probs; launch_gemm(tmp.data(), c.batch, st, s, &scr); }
     cudaEventRecord(e0, s);
-    for (int r = 0; r < reps; ++r) { tmp = probs; launch_gemm(tmp.data(), c.batch, st, s); }
+    for (int r = 0; r < reps; ++r) { tmp = probs; launch_gemm(tmp.data(), c.batch, st, s, &scr); }
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
@@ -117,7 +133,9 @@ int main(int argc, char** argv) {
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&msr, e0, e1);
-    const double fl = 8.0 * c.M * c.N * (double)c.K * c.batch;
+    const double fl = (c.sym ? 4.0 * c.M * (c.M + 1.0) : 8.0 * c.M * c.N) * (double)c.K * c.batch;
+    cudaDeviceSynchronize();
+    scr.release();
     printf("%s\n {\"case\": \"%s\", \"rel_err\": %.3e, \"ms\": %.4f, \"tflops\": %.2f, \"cublas_ms\": %.4f, "
            "\"cublas_tflops\": %.2f}",
            first ? "" : ",", c.name, std::sqrt(num / den), ms / reps, fl / (ms / reps) / 1e9, msr / reps,
