@@ -104,24 +104,41 @@ __device__ __forceinline__ int find_estart(const P* p, int n, int idx) {
 constexpr int FUSED_MAX_N = 256;   // lower-triangle fused path (per-lane column accumulators)
 constexpr int SMEM_MAX_N = 144;    // matrix (packed lower triangle) resident in shared memory
 
+// Shared-memory budget of the fused path: the fixed vectors, then as many trailing rows of the
+// packed lower triangle as fit (rows >= r0 live in shared memory, rows < r0 stay in global /
+// L2).  The trailing rows are touched by every step, the leading ones only by the first r0
+// steps, so keeping the tail on chip removes most of the L2 traffic (n = 192: r0 ~ 118, the
+// global part is (118/192)^3 ~ 23% of a full-L2 reduction).
+constexpr size_t FUSED_SMEM_BUDGET = 220u << 10;
+__host__ __device__ inline size_t fused_base_bytes(int n) { return (size_t)n * 16 * 2 + (size_t)16 * (3 + 8) * n + 64; }
+// Measured (config 3, n = 192): the reduction is latency-bound (fixed-latency FP64 chains,
+// barriers), not L2-bound, and a partial shared-memory tail costs the second resident CTA per
+// SM; so only matrices that fit entirely (n <= SMEM_MAX_N) go on chip.
+__host__ __device__ inline int fused_r0(int n) {
+  if (n > 144) return n;
+  const size_t avail = (FUSED_SMEM_BUDGET - fused_base_bytes(n)) / 16;   // complex entries
+  int r0 = 0;
+  while ((size_t)n * (n + 1) / 2 - (size_t)r0 * (r0 + 1) / 2 > avail) ++r0;
+  return r0;
+}
+
 // Householder tridiagonalisation (zhetd2, lower) touching only the lower triangle, with the
 // rank-2 update of step j-1 fused into the Hermitian mat-vec of step j: one read-modify-write
-// pass over the trailing triangle per step.  SM: the packed triangle lives in shared memory.
+// pass over the trailing triangle per step.  Rows >= r0 of the packed triangle live in shared
+// memory (r0 = 0: all of it), rows < r0 in the global A.
 // Reflector j is written to row j (columns > j) of the global A for the back-transform.
-template <bool SM>
-__device__ void tridiag_fused(cplx* __restrict__ A, const int n, cplx* vcur, cplx* wcur, cplx* base, double* dvec,
-                              double* evec, cplx* tau_out, double2* red) {
+__device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, cplx* vcur, cplx* wcur, cplx* base,
+                              double* dvec, double* evec, cplx* tau_out, double2* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   cplx* vprev = base;
   cplx* wprev = vprev + n;
   cplx* prow = wprev + n;
   cplx* colpart = prow + n;                   // [HEEV_WARPS][n]
   cplx* Ap = colpart + HEEV_WARPS * n;        // packed lower triangle (SM)
-#define LL(r, c) (SM ? Ap[(size_t)(r) * ((r) + 1) / 2 + (c)] : A[(size_t)(r) * n + (c)])
-  if (SM) {
-    for (int r = warp; r < n; r += HEEV_WARPS)
-      for (int c = lane; c <= r; c += 32) Ap[(size_t)r * (r + 1) / 2 + c] = A[(size_t)r * n + c];
-  }
+  const size_t pbase = (size_t)r0 * (r0 + 1) / 2;
+#define LL(r, c) (*((r) >= r0 ? &Ap[(size_t)(r) * ((r) + 1) / 2 - pbase + (c)] : &A[(size_t)(r) * n + (c)]))
+  for (int r = r0 + warp; r < n; r += HEEV_WARPS)
+    for (int c = lane; c <= r; c += 32) Ap[(size_t)r * (r + 1) / 2 - pbase + c] = A[(size_t)r * n + c];
   for (int i = tid; i < n; i += HEEV_THREADS) {
     vprev[i] = make_double2(0.0, 0.0);
     wprev[i] = make_double2(0.0, 0.0);
@@ -401,8 +418,7 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* 
   double tr = 0.0;
   for (int i = tid; i < n; i += HEEV_THREADS) tr += A[(size_t)i * n + i].x;
   const double trace = block_sum2(tr, 0.0, red).x;
-  if (n <= SMEM_MAX_N) tridiag_fused<true>(A, n, sv, sp, base, dvec, evec, P.tau, red);
-  else if (n <= FUSED_MAX_N) tridiag_fused<false>(A, n, sv, sp, base, dvec, evec, P.tau, red);
+  if (n <= FUSED_MAX_N) tridiag_fused(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
   else tridiag_full(A, n, sv, sp, dvec, evec, P.tau, red);
   tridiag_stats(P, trace);
 }
@@ -1130,10 +1146,9 @@ size_t heev_work_doubles(int n, int kmax) {
 
 size_t heev_smem_bytes(int n, int kmax) {
   (void)kmax;
-  size_t b = (size_t)n * 16 * 2;
-  if (n <= FUSED_MAX_N) b += (size_t)16 * (3 + HEEV_WARPS) * n;
-  if (n <= SMEM_MAX_N) b += (size_t)16 * n * (n + 1) / 2;
-  return b + 64;
+  if (n > FUSED_MAX_N) return (size_t)n * 16 * 2 + 64;
+  const int r0 = fused_r0(n);
+  return fused_base_bytes(n) + 16 * ((size_t)n * (n + 1) / 2 - (size_t)r0 * (r0 + 1) / 2);
 }
 
 int heev_max_n() { return HEEV_MAX_N; }
@@ -1175,8 +1190,7 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   static bool attr = false;
   if (!attr) {
-    size_t mx = std::max(heev_smem_bytes(SMEM_MAX_N, 1), heev_smem_bytes(HEEV_MAX_N, 1));
-    cudaFuncSetAttribute(heev_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(heev_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
     attr = true;
   }
   int total = 0;
