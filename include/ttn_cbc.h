@@ -41,7 +41,8 @@ typedef enum {
   TTN_ERR_OOM = 4,          /* device or pinned-host allocation failed                       */
   TTN_ERR_CUDA = 5,         /* a CUDA runtime call or kernel launch failed                   */
   TTN_ERR_NUMERIC = 6,      /* non-finite values, eigensolver / Cholesky breakdown            */
-  TTN_ERR_UNSUPPORTED = 7   /* a size beyond the compiled limits (see ttn_last_error)        */
+  TTN_ERR_UNSUPPORTED = 7,  /* a size beyond the compiled limits (see ttn_last_error)        */
+  TTN_ERR_NCCL = 8          /* NCCL missing or a collective failed (multi-GPU apply)          */
 } ttn_status;
 
 typedef enum { TTN_STATE = 0, TTN_OPERATOR = 1 } ttn_kind;
@@ -129,6 +130,35 @@ TTN_API ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const
 TTN_API ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out);
 /* Batched overlaps <a_j|b_j>, j < n.                                                      */
 TTN_API ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b, ttn_c128* out);
+/* ---------------------------------------------------------------- multi-GPU            */
+/* 128-byte NCCL unique id for a new communicator: create it on one rank and hand the same
+ * bytes to every rank (e.g. by a torch.distributed broadcast).  NCCL is loaded at run time
+ * (libnccl.so.2).  Errors: NCCL.                                                          */
+TTN_API ttn_status ttn_comm_unique_id(void* out128);
+/* Make ctx rank `rank` of a `world`-rank communicator (one process per GPU, NCCL over
+ * NVLink / NVSwitch) and split every later cbc_apply / cbc_apply_batch on it into
+ * `parts` >= world subtree groups (SURVEY §8(e) mechanism 2, B:5 (e), B:10):
+ *  - the tree is cut below a replicated top: starting from the root's child subtrees, the
+ *    largest subtree is replaced by its children until there are >= parts subtrees; the
+ *    subtrees are dealt to the groups by size (largest first, to the lightest group) and
+ *    group g belongs to rank g % world;
+ *  - every rank passes the SAME op and state (replicated inputs) and receives the full result;
+ *  - per apply: each rank runs the up-sweep (Eq. 10) of its subtrees; the subtree roots'
+ *    up-factors (boundary environments) are broadcast from their owners; the top is swept
+ *    up and down on every rank (replicated); each rank runs the down-sweep (Eq. 11) and the
+ *    final sweep (Eqs. 12-14) of its subtrees; the subtree roots' R factors and every
+ *    subtree's new tensors are broadcast; the top's final sweep closes the apply.
+ *    The sequence of collectives depends only on the tree, never on data, so all ranks
+ *    issue them in the same order.
+ * world = 1 with parts > 1 runs the same partitioned schedule on one GPU (all groups local,
+ * 1-rank NCCL collectives): the single-GPU check of the schedule.  unique_id128 = NULL
+ * detaches the communicator (plain applies).  Errors: ARG, NCCL.                          */
+TTN_API ttn_status ttn_ctx_set_comm(ttn_ctx ctx, const void* unique_id128, int rank, int world, int parts);
+/* The partition ttn_ctx_set_comm would use (host-only, no device needed): group_out[i] = -1
+ * for nodes of the replicated top, else the subtree group of node i (rank = group % world).
+ * Errors: ARG, TOPOLOGY.                                                                  */
+TTN_API ttn_status ttn_partition_plan(int32_t n_nodes, const int32_t* parent, int parts, int32_t* group_out);
+
 /* ---------------------------------------------------------------- measurement          */
 /* Process-wide kernel-family timing with CUDA events on the launching stream (used by
  * bench.py for the roofline).  on = 1 resets and enables, 0 disables.                    */

@@ -197,3 +197,50 @@ def ttn_norm(ctx: Context, a: TTN) -> float:
     v = C.c_double()
     L.check(ctx.h, L.load().ttn_norm(ctx.h, a.h, C.byref(v)))
     return v.value
+
+
+# ---------------------------------------------------------------- multi-GPU (NCCL)
+def ttn_comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (create on one rank, share the bytes with the others)."""
+    buf = C.create_string_buffer(128)
+    L.check(None, L.load().ttn_comm_unique_id(buf))
+    return buf.raw
+
+
+def ttn_ctx_set_comm(ctx: Context, unique_id: Optional[bytes], rank: int = 0, world: int = 1, parts: int = 1) -> None:
+    """Make ctx one rank of a partitioned multi-GPU apply (include/ttn_cbc.h); None detaches."""
+    if unique_id is None:
+        L.check(ctx.h, L.load().ttn_ctx_set_comm(ctx.h, None, 0, 1, 1))
+        return
+    buf = C.create_string_buffer(bytes(unique_id), 128)
+    L.check(ctx.h, L.load().ttn_ctx_set_comm(ctx.h, buf, int(rank), int(world), int(parts)))
+
+
+def ttn_partition_plan(parent: Sequence[int], parts: int) -> List[int]:
+    """Subtree groups of a parts-way partitioned apply (-1: replicated top); host-only."""
+    n = len(parent)
+    out = (C.c_int32 * n)()
+    L.check(None, L.load().ttn_partition_plan(n, L.as_i32(parent), int(parts), out))
+    return list(out)
+
+
+def share_bytes(payload: Optional[bytes], nbytes: int = 128, group=None) -> bytes:
+    """Broadcast `nbytes` bytes from rank 0 of a torch.distributed group (gloo or nccl):
+    the transport of the NCCL unique id (torch is plumbing only)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.zeros(nbytes, dtype=torch.uint8)
+    if dist.get_rank(group) == 0:
+        t[:] = torch.tensor(list(payload), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda(torch.cuda.current_device())
+    dist.broadcast(t, src=0, group=group)
+    return bytes(t.cpu().tolist())
+
+
+def comm_bootstrap(ctx: Context, parts: Optional[int] = None, group=None) -> None:
+    """Attach a NCCL communicator over the ranks of the initialised torch.distributed group."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = share_bytes(ttn_comm_unique_id() if rank == 0 else None, 128, group)
+    ttn_ctx_set_comm(ctx, uid, rank, world, parts or world)

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libttncbc.so")
-SOURCES = ["gemm.cu", "heev.cu", "chfsi.cu", "chol.cu", "misc.cu", "prof.cpp", "contract.cpp", "cbc.cpp", "runtime.cpp", "api.cpp"]
+SOURCES = ["gemm.cu", "heev.cu", "chfsi.cu", "chol.cu", "misc.cu", "prof.cpp", "comm.cpp", "contract.cpp", "cbc.cpp", "runtime.cpp", "api.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             print(out.decode(), file=sys.stderr)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout + r.stderr)

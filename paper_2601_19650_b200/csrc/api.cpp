@@ -84,6 +84,7 @@ ttn_status ttn_ctx_destroy(ttn_ctx ctx) {
   ctx->scratch.release();
   ctx->env.release();
   delete ctx->stager;
+  delete ctx->comm;
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
   delete ctx;
   return TTN_OK;
@@ -215,6 +216,36 @@ ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b,
 }
 
 ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out) { return ttn_overlap_batch(ctx, 1, &a, &b, out); }
+
+ttn_status ttn_comm_unique_id(void* out128) {
+  if (!out128) return TTN_ERR_ARG;
+  return guard(nullptr, [&] { comm_unique_id(out128); });
+}
+
+ttn_status ttn_ctx_set_comm(ttn_ctx ctx, const void* unique_id128, int rank, int world, int parts) {
+  if (!ctx) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx->comm;
+    ctx->comm = nullptr;
+    ctx->parts = 1;
+    if (!unique_id128) return;
+    if (world < 1 || rank < 0 || rank >= world || parts < world) throw Error(TTN_ERR_ARG, "need 0 <= rank < world <= parts");
+    ctx->comm = comm_create(unique_id128, rank, world, ctx->device);
+    ctx->parts = parts;
+  });
+}
+
+ttn_status ttn_partition_plan(int32_t n_nodes, const int32_t* parent, int parts, int32_t* group_out) {
+  if (!parent || !group_out || n_nodes < 1 || parts < 1) return TTN_ERR_ARG;
+  return guard(nullptr, [&] {
+    ttn_s t;
+    build_topology(&t, parent, n_nodes);
+    std::vector<int> g = partition_groups(&t, parts, nullptr);
+    for (int i = 0; i < n_nodes; ++i) group_out[i] = g[i];
+  });
+}
 
 ttn_status ttn_profile_enable(int on) {
   prof_enable(on != 0);

@@ -276,6 +276,73 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
 
 }  // namespace
 
+// Subtree partition of a multi-GPU apply (ttn_ctx_set_comm; SURVEY §8(e) mechanism 2).
+// group[i] = -1: node of the replicated top (always the root); else the subtree group.
+struct Partition {
+  bool on = false;
+  int world = 1, rank = 0;
+  std::vector<int> group;
+  std::vector<int> cuts;     // subtree roots (their parent is a top node)
+  bool top(int i) const { return group[i] < 0; }
+  bool mine(int i) const { return group[i] < 0 || group[i] % world == rank; }
+  int owner(int i) const { return group[i] % world; }
+};
+
+// subtree groups of a `parts`-way partition (host-only; also exported as ttn_partition_plan)
+std::vector<int> partition_groups(const ttn_s* ref, int parts, std::vector<int>* cuts_out) {
+  const int n = ref->n;
+  std::vector<int> group(n, -1);
+  if (parts <= 1) return group;
+  const auto& ch = ref->children;
+  // subtree sizes (nodes in post-order: deepest first)
+  std::vector<int> order(n), size(n, 1);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int x, int y) { return ref->depth[x] > ref->depth[y]; });
+  for (int i : order)
+    if (ref->parent[i] >= 0) size[ref->parent[i]] += size[i];
+  std::vector<int> units(ch[ref->root].begin(), ch[ref->root].end());
+  while ((int)units.size() < parts) {   // expand the largest subtree that branches (>= 2 children)
+    int best = -1;
+    for (size_t u = 0; u < units.size(); ++u)
+      if (ch[units[u]].size() >= 2 && (best < 0 || size[units[u]] > size[units[best]] ||
+                                    (size[units[u]] == size[units[best]] && units[u] < units[best])))
+        best = (int)u;
+    if (best < 0) break;
+    const int x = units[best];
+    units.erase(units.begin() + best);
+    units.insert(units.end(), ch[x].begin(), ch[x].end());
+  }
+  std::sort(units.begin(), units.end(), [&](int x, int y) { return size[x] != size[y] ? size[x] > size[y] : x < y; });
+  std::vector<long long> load(parts, 0);
+  for (int u : units) {
+    const int g = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    load[g] += size[u];
+    std::vector<int> st{u};
+    while (!st.empty()) {
+      const int x = st.back();
+      st.pop_back();
+      group[x] = g;
+      for (int c : ch[x]) st.push_back(c);
+    }
+  }
+  if (cuts_out) {
+    *cuts_out = units;
+    std::sort(cuts_out->begin(), cuts_out->end());
+  }
+  return group;
+}
+
+Partition make_partition(const ttn_s* ref, const ttn_ctx_s* ctx) {
+  Partition P;
+  P.group.assign(ref->n, -1);
+  if (!ctx->comm || ctx->parts <= 1) return P;
+  P.on = true;
+  P.world = ctx->comm->world;
+  P.rank = ctx->comm->rank;
+  P.group = partition_groups(ref, ctx->parts, &P.cuts);
+  return P;
+}
+
 void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts, int64_t max_bond,
                     double tol, ttn_s** outs, ttn_cbc_report* reps) {
   auto t0 = std::chrono::steady_clock::now();
@@ -309,83 +376,152 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       used[i] = (ch[p].size() >= 2) || used[p];
     }
   }
+  const Partition part = make_partition(ref, ctx);
+  Comm* comm = part.on ? ctx->comm : nullptr;
   ctx->env.reset();
   ctx->scratch.reset();
   ctx->host_syncs = 0;
   ExecStats st;
-  std::vector<double> w_inst(nb, 0.0), flops_inst(nb, 0.0);
-  std::vector<int> fb_inst(nb, 0);
+  // per-instance accumulators: replicated top work counted on every rank, subtree work only
+  // on its owner (summed over ranks at the end)
+  std::vector<double> w_inst(nb, 0.0), flops_inst(nb, 0.0), w_sub(nb, 0.0), flops_sub(nb, 0.0);
+  std::vector<int> fb_inst(nb, 0), fb_sub(nb, 0);
   std::vector<Fac> up((size_t)nb * n), down((size_t)nb * n), R((size_t)nb * n);
   // trivial factor L^{[(-,r)]} = 1 (extent-1 legs)
   cplx* one = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx)));
   launch_fill(one, 1, make_double2(1.0, 0.0), ctx->stream);
   for (int b = 0; b < nb; ++b) down[(size_t)b * n + root] = Fac{one, 1, 1, 1};
 
-  // ---------------- 1. up-sweep (Eq. 10)
-  for (int L = maxd; L >= 1; --L) {
-    std::vector<Task> tasks;
-    std::vector<CompressJob> jobs;
-    for (int b = 0; b < nb; ++b)
-      for (int i = 0; i < n; ++i) {
-        if (ref->depth[i] != L || !used[i]) continue;
-        std::map<int, const Fac*> f;
-        for (size_t l = 0; l < ch[i].size(); ++l) f[1 + (int)l] = &up[(size_t)b * n + ch[i][l]];
-        tasks.push_back(node_task(sts[b], ops[b], i, f, 0, nullptr));
-        jobs.push_back(CompressJob{nullptr, 0, 0, &up[(size_t)b * n + i], sts[b]->shape[i][1], ops[b]->shape[i][2], b});
-      }
-    if (tasks.empty()) continue;
-    ExecStats cs;
-    contract_batch(ctx, tasks, cs);
-    for (size_t j = 0; j < tasks.size(); ++j) {
-      int64_t tot = 1;
-      for (auto d : tasks[j].out_dims) tot *= d;
-      jobs[j].X = tasks[j].out;
-      jobs[j].n = jobs[j].a * jobs[j].b;
-      jobs[j].m = tot / jobs[j].n;
-    }
-    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-    // per-instance flop share of the contraction (uniform tasks per instance)
-    for (size_t j = 0; j < jobs.size(); ++j) flops_inst[jobs[j].inst] += tasks[j].flops;
-    st.flops += cs.flops;
-    compress_batch(ctx, jobs, max_bond, tol, st, w_inst, flops_inst);
-    ctx->scratch.reset();
-  }
+  auto acc_w = [&](bool sub) -> std::vector<double>& { return sub ? w_sub : w_inst; };
+  auto acc_f = [&](bool sub) -> std::vector<double>& { return sub ? flops_sub : flops_inst; };
 
-  // ---------------- 2. down-sweep (Eq. 11)
-  for (int L = 0; L < maxd; ++L) {
-    std::vector<Task> tasks;
-    std::vector<CompressJob> jobs;
-    for (int b = 0; b < nb; ++b)
-      for (int i = 0; i < n; ++i) {
-        if (ref->depth[i] != L) continue;
-        for (size_t lk = 0; lk < ch[i].size(); ++lk) {
-          int k = ch[i][lk];
+  // ---------------- 1. up-sweep (Eq. 10) over the nodes selected by `sel`, deepest level first
+  auto up_sweep = [&](auto sel, bool sub) {
+    for (int L = maxd; L >= 1; --L) {
+      std::vector<Task> tasks;
+      std::vector<CompressJob> jobs;
+      for (int b = 0; b < nb; ++b)
+        for (int i = 0; i < n; ++i) {
+          if (ref->depth[i] != L || !used[i] || !sel(i)) continue;
           std::map<int, const Fac*> f;
-          f[0] = &down[(size_t)b * n + i];
-          for (size_t l = 0; l < ch[i].size(); ++l)
-            if (l != lk) f[1 + (int)l] = &up[(size_t)b * n + ch[i][l]];
-          tasks.push_back(node_task(sts[b], ops[b], i, f, 1 + (int)lk, nullptr));
-          jobs.push_back(CompressJob{nullptr, 0, 0, &down[(size_t)b * n + k], sts[b]->shape[k][1], ops[b]->shape[k][2], b});
+          for (size_t l = 0; l < ch[i].size(); ++l) f[1 + (int)l] = &up[(size_t)b * n + ch[i][l]];
+          tasks.push_back(node_task(sts[b], ops[b], i, f, 0, nullptr));
+          jobs.push_back(CompressJob{nullptr, 0, 0, &up[(size_t)b * n + i], sts[b]->shape[i][1], ops[b]->shape[i][2], b});
         }
+      if (tasks.empty()) continue;
+      ExecStats cs;
+      contract_batch(ctx, tasks, cs);
+      for (size_t j = 0; j < tasks.size(); ++j) {
+        int64_t tot = 1;
+        for (auto d : tasks[j].out_dims) tot *= d;
+        jobs[j].X = tasks[j].out;
+        jobs[j].n = jobs[j].a * jobs[j].b;
+        jobs[j].m = tot / jobs[j].n;
       }
-    if (tasks.empty()) continue;
-    ExecStats cs;
-    contract_batch(ctx, tasks, cs);
-    for (size_t j = 0; j < tasks.size(); ++j) {
-      int64_t tot = 1;
-      for (auto d : tasks[j].out_dims) tot *= d;
-      jobs[j].X = tasks[j].out;
-      jobs[j].n = jobs[j].a * jobs[j].b;
-      jobs[j].m = tot / jobs[j].n;
+      st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+      for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst] += tasks[j].flops;
+      st.flops += cs.flops;
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub));
+      ctx->scratch.reset();
     }
-    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-    for (size_t j = 0; j < jobs.size(); ++j) flops_inst[jobs[j].inst] += tasks[j].flops;
-    st.flops += cs.flops;
-    compress_batch(ctx, jobs, max_bond, tol, st, w_inst, flops_inst);
-    ctx->scratch.reset();
+  };
+  // ---------------- 2. down-sweep (Eq. 11): nodes selected by `sel` give their children factors
+  auto down_sweep = [&](auto sel, bool sub) {
+    for (int L = 0; L < maxd; ++L) {
+      std::vector<Task> tasks;
+      std::vector<CompressJob> jobs;
+      for (int b = 0; b < nb; ++b)
+        for (int i = 0; i < n; ++i) {
+          if (ref->depth[i] != L || !sel(i)) continue;
+          for (size_t lk = 0; lk < ch[i].size(); ++lk) {
+            int k = ch[i][lk];
+            std::map<int, const Fac*> f;
+            f[0] = &down[(size_t)b * n + i];
+            for (size_t l = 0; l < ch[i].size(); ++l)
+              if (l != lk) f[1 + (int)l] = &up[(size_t)b * n + ch[i][l]];
+            tasks.push_back(node_task(sts[b], ops[b], i, f, 1 + (int)lk, nullptr));
+            jobs.push_back(CompressJob{nullptr, 0, 0, &down[(size_t)b * n + k], sts[b]->shape[k][1], ops[b]->shape[k][2], b});
+          }
+        }
+      if (tasks.empty()) continue;
+      ExecStats cs;
+      contract_batch(ctx, tasks, cs);
+      for (size_t j = 0; j < tasks.size(); ++j) {
+        int64_t tot = 1;
+        for (auto d : tasks[j].out_dims) tot *= d;
+        jobs[j].X = tasks[j].out;
+        jobs[j].n = jobs[j].a * jobs[j].b;
+        jobs[j].m = tot / jobs[j].n;
+      }
+      st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+      for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst] += tasks[j].flops;
+      st.flops += cs.flops;
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub));
+      ctx->scratch.reset();
+    }
+  };
+  // rank-owned integers (factor ranks) made global: owners fill, zeros elsewhere, sum
+  auto share_ints = [&](std::vector<int>& v) {
+    if (!comm || v.empty()) return;
+    int* d = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * v.size()));
+    TTN_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, ctx->stream));
+    comm->allreduce_sum(d, v.size(), ctx->stream);
+    TTN_CUDA(cudaMemcpyAsync(v.data(), d, sizeof(int) * v.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  };
+  // broadcast factors `F[b*n + u]` of the cut nodes from their owners (ranks k shared first)
+  auto share_factors = [&](std::vector<Fac>& F, bool only_used) {
+    if (!part.on) return;
+    std::vector<int> ks;
+    for (int b = 0; b < nb; ++b)
+      for (int u : part.cuts) {
+        if (only_used && !used[u]) continue;
+        const Fac& f = F[(size_t)b * n + u];
+        ks.push_back(part.owner(u) == part.rank ? (int)f.k : 0);
+      }
+    share_ints(ks);
+    size_t q = 0;
+    comm->group_start();
+    for (int b = 0; b < nb; ++b)
+      for (int u : part.cuts) {
+        if (only_used && !used[u]) continue;
+        Fac& f = F[(size_t)b * n + u];
+        const int k = ks[q++];
+        if (part.owner(u) != part.rank) {
+          f.k = k;
+          f.a = sts[b]->shape[u][1];
+          f.b = ops[b]->shape[u][2];
+          f.p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * std::max<int64_t>(f.k * f.a * f.b, 1)));
+        }
+        comm->bcast(f.p, sizeof(cplx) * f.k * f.a * f.b, part.owner(u), ctx->stream);
+      }
+    comm->group_end();
+  };
+
+  auto in_sub = [&](int i) { return !part.top(i) && part.mine(i); };
+  auto in_top = [&](int i) { return part.top(i); };
+  // up-sweep: subtrees (rank-local), boundary environments, replicated top
+  if (part.on) {
+    up_sweep(in_sub, true);
+    share_factors(up, true);
   }
+  up_sweep(in_top, false);
+  // down-sweep: replicated top (gives the subtree roots their down factors), then subtrees
+  down_sweep(in_top, false);
+  if (part.on) down_sweep(in_sub, true);
 
   // ---------------- output shapes: r_i = min(d_i prod_c r_c, kd_i); root 1
+  if (part.on) {   // subtree nodes' down ranks (kd) from their owners
+    std::vector<int> kd;
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < n; ++i)
+        if (!part.top(i) && i != root) kd.push_back(part.mine(i) ? (int)down[(size_t)b * n + i].k : 0);
+    share_ints(kd);
+    size_t q = 0;
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < n; ++i)
+        if (!part.top(i) && i != root) down[(size_t)b * n + i].k = kd[q++];
+  }
   std::vector<std::vector<int64_t>> rb(nb, std::vector<int64_t>(n, 1));
   {
     std::vector<int> order(n);
@@ -401,66 +537,82 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   }
   for (int b = 0; b < nb; ++b) outs[b] = new_ttn_like(ctx, ref, TTN_STATE, rb[b]);
 
-  // ---------------- 3. final sweep (Eqs. 12-14) and 4. assembly
-  for (int L = maxd; L >= 0; --L) {
-    std::vector<Task> tasks;
-    std::vector<std::pair<int, int>> who;
-    for (int b = 0; b < nb; ++b)
-      for (int i = 0; i < n; ++i) {
-        if (ref->depth[i] != L) continue;
-        std::map<int, const Fac*> f;
-        for (size_t l = 0; l < ch[i].size(); ++l) f[1 + (int)l] = &R[(size_t)b * n + ch[i][l]];
-        cplx* out = (i == root) ? outs[b]->node(i) : nullptr;   // assembly: T'_root = Z_root
-        tasks.push_back(node_task(sts[b], ops[b], i, f, 0, out));
-        who.push_back({b, i});
+  // ---------------- 3. final sweep (Eqs. 12-14) and 4. assembly, over the nodes selected
+  auto final_sweep = [&](auto sel, bool sub) {
+    for (int L = maxd; L >= 0; --L) {
+      std::vector<Task> tasks;
+      std::vector<std::pair<int, int>> who;
+      for (int b = 0; b < nb; ++b)
+        for (int i = 0; i < n; ++i) {
+          if (ref->depth[i] != L || !sel(i)) continue;
+          std::map<int, const Fac*> f;
+          for (size_t l = 0; l < ch[i].size(); ++l) f[1 + (int)l] = &R[(size_t)b * n + ch[i][l]];
+          cplx* out = (i == root) ? outs[b]->node(i) : nullptr;   // assembly: T'_root = Z_root
+          tasks.push_back(node_task(sts[b], ops[b], i, f, 0, out));
+          who.push_back({b, i});
+        }
+      if (tasks.empty()) continue;
+      ExecStats cs;
+      contract_batch(ctx, tasks, cs);
+      st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+      for (size_t j = 0; j < who.size(); ++j) acc_f(sub)[who[j].first] += tasks[j].flops;
+      st.flops += cs.flops;
+      std::vector<GemmProblem> sg, rg;
+      std::vector<QRJob> qj;
+      std::vector<PermProblem> pq;
+      for (size_t j = 0; j < tasks.size(); ++j) {
+        const int b = who[j].first, i = who[j].second;
+        if (i == root) continue;
+        const Fac& fd = down[(size_t)b * n + i];
+        const int64_t nz = fd.a * fd.b;
+        int64_t tot = 1;
+        for (auto d : tasks[j].out_dims) tot *= d;
+        const int64_t ms = tot / nz, kd = fd.k, r = rb[b][i];
+        cplx* S = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * kd));
+        sg.push_back(mk_gemm(tasks[j].out, OP_N, nz, fd.p, OP_T, nz, S, kd, ms, kd, nz));   // S = Z Fd^T (Eq. 12 via Z)
+        acc_f(sub)[b] += 8.0 * (double)ms * kd * nz;
+        cplx* Q = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * r));
+        qj.push_back(QRJob{S, ms, kd, Q, b});
+        // T'_i = Q in ABI order [d, r, r_c...]: Q viewed as [d, Rc, r] -> [d, r, Rc]
+        const int64_t d = ref->phys[i], Rc = ms / d;
+        PermProblem pp{};
+        pp.src = Q; pp.dst = outs[b]->node(i); pp.rank = 3; pp.conj = 0;
+        pp.dims[0] = d; pp.dims[1] = r; pp.dims[2] = Rc;
+        pp.sstride[0] = Rc * r; pp.sstride[1] = 1; pp.sstride[2] = r;
+        pp.total = d * r * Rc;
+        pq.push_back(pp);
+        // R_i = Q^H Z  (Eq. 14 with Q*, reading A6)
+        Fac& Ri = R[(size_t)b * n + i];
+        Ri.p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * r * nz));
+        Ri.k = r; Ri.a = fd.a; Ri.b = fd.b;
+        rg.push_back(mk_gemm(Q, OP_C, r, tasks[j].out, OP_N, nz, Ri.p, nz, r, nz, ms));
+        acc_f(sub)[b] += 8.0 * (double)r * nz * ms;
       }
-    ExecStats cs;
-    contract_batch(ctx, tasks, cs);
-    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-    for (size_t j = 0; j < who.size(); ++j) flops_inst[who[j].first] += tasks[j].flops;
-    st.flops += cs.flops;
-    std::vector<GemmProblem> sg, rg;
-    std::vector<QRJob> qj;
-    std::vector<PermProblem> pq;
-    std::vector<std::pair<size_t, int64_t>> rinfo;
-    for (size_t j = 0; j < tasks.size(); ++j) {
-      const int b = who[j].first, i = who[j].second;
-      if (i == root) continue;
-      const Fac& fd = down[(size_t)b * n + i];
-      const int64_t nz = fd.a * fd.b;
-      int64_t tot = 1;
-      for (auto d : tasks[j].out_dims) tot *= d;
-      const int64_t ms = tot / nz, kd = fd.k, r = rb[b][i];
-      cplx* S = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * kd));
-      sg.push_back(mk_gemm(tasks[j].out, OP_N, nz, fd.p, OP_T, nz, S, kd, ms, kd, nz));   // S = Z Fd^T (Eq. 12 via Z)
-      flops_inst[b] += 8.0 * (double)ms * kd * nz;
-      cplx* Q = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * r));
-      qj.push_back(QRJob{S, ms, kd, Q, b});
-      // T'_i = Q in ABI order [d, r, r_c...]: Q viewed as [d, Rc, r] -> [d, r, Rc]
-      const int64_t d = ref->phys[i], Rc = ms / d;
-      PermProblem pp{};
-      pp.src = Q; pp.dst = outs[b]->node(i); pp.rank = 3; pp.conj = 0;
-      pp.dims[0] = d; pp.dims[1] = r; pp.dims[2] = Rc;
-      pp.sstride[0] = Rc * r; pp.sstride[1] = 1; pp.sstride[2] = r;
-      pp.total = d * r * Rc;
-      pq.push_back(pp);
-      // R_i = Q^H Z  (Eq. 14 with Q*, reading A6)
-      Fac& Ri = R[(size_t)b * n + i];
-      Ri.p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * r * nz));
-      Ri.k = r; Ri.a = fd.a; Ri.b = fd.b;
-      rg.push_back(mk_gemm(Q, OP_C, r, tasks[j].out, OP_N, nz, Ri.p, nz, r, nz, ms));
-      flops_inst[b] += 8.0 * (double)r * nz * ms;
+      gemm_batch(ctx, sg, st);
+      qr_batch(ctx, qj, st, acc_f(sub), sub ? fb_sub : fb_inst);
+      if (!pq.empty()) launch_permute(pq.data(), (int)pq.size(), *ctx->stager, ctx->stream);
+      gemm_batch(ctx, rg, st);
+      ctx->scratch.reset();
     }
-    gemm_batch(ctx, sg, st);
-    qr_batch(ctx, qj, st, flops_inst, fb_inst);
-    if (!pq.empty()) launch_permute(pq.data(), (int)pq.size(), *ctx->stager, ctx->stream);
-    gemm_batch(ctx, rg, st);
-    ctx->scratch.reset();
+  };
+  if (part.on) {
+    final_sweep(in_sub, true);
+    share_factors(R, false);   // subtree roots' R^{[u]} (Eq. 14) for the top's final sweep
+    comm->group_start();       // every subtree's new tensors to every rank
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < n; ++i)
+        if (!part.top(i)) {
+          int64_t e = 1;
+          for (auto d : outs[b]->shape[i]) e *= d;
+          comm->bcast(outs[b]->node(i), sizeof(cplx) * e, part.owner(i), ctx->stream);
+        }
+    comm->group_end();
   }
+  final_sweep(in_top, false);
 
-  // ---------------- report: ||phi|| = ||T'_root||_F
+  // ---------------- report: ||phi|| = ||T'_root||_F; subtree totals summed over ranks
   std::vector<SumsqProblem> sq(nb);
-  double* d_sq = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nb));
+  double* d_sq = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nb * 4));
   for (int b = 0; b < nb; ++b) {
     sq[b].x = outs[b]->node(root);
     sq[b].len = 1;
@@ -468,6 +620,23 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
     sq[b].out = d_sq + b;
   }
   launch_sumsq(sq.data(), nb, *ctx->stager, ctx->stream);
+  if (part.on) {
+    std::vector<double> h(3 * (size_t)nb);
+    for (int b = 0; b < nb; ++b) {
+      h[b] = w_sub[b];
+      h[nb + b] = flops_sub[b];
+      h[2 * nb + b] = fb_sub[b];
+    }
+    TTN_CUDA(cudaMemcpyAsync(d_sq + nb, h.data(), sizeof(double) * 3 * nb, cudaMemcpyHostToDevice, ctx->stream));
+    comm->allreduce_sum(d_sq + nb, 3 * (size_t)nb, ctx->stream);
+    TTN_CUDA(cudaMemcpyAsync(h.data(), d_sq + nb, sizeof(double) * 3 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    for (int b = 0; b < nb; ++b) {
+      w_inst[b] += h[b];
+      flops_inst[b] += h[nb + b];
+      fb_inst[b] += (int)std::lround(h[2 * nb + b]);
+    }
+  }
   ctx->ensure_small(sizeof(double) * nb);
   double* hs = reinterpret_cast<double*>(ctx->hbuf);
   TTN_CUDA(cudaMemcpyAsync(hs, d_sq, sizeof(double) * nb, cudaMemcpyDeviceToHost, ctx->stream));

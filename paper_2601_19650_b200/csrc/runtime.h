@@ -2,6 +2,7 @@
 // and the status plumbing behind the C ABI (include/ttn_cbc.h).
 #pragma once
 #include "../../include/ttn_cbc.h"
+#include "comm.h"
 #include "kernels.h"
 
 #include <cuda_runtime.h>
@@ -72,6 +73,8 @@ struct ttn_ctx_s {
   char* dbuf = nullptr;    // device mirror of small results
   size_t dbuf_size = 0;
   int host_syncs = 0;
+  tcbc::Comm* comm = nullptr;   // multi-GPU apply (ttn_ctx_set_comm)
+  int parts = 1;                // subtree groups of a partitioned apply
   void sync();             // cudaStreamSynchronize + stager epoch
   void ensure_small(size_t bytes);
 };
@@ -104,5 +107,8 @@ void free_ttn(ttn_s* t);
 void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts,
                     int64_t max_bond, double tol, ttn_s** outs, ttn_cbc_report* reps);
 void overlap_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* a, const ttn_s* const* b, cplx* out);
+// Subtree groups of a parts-way partitioned apply (group -1: replicated top); cuts_out gets
+// the subtree roots.  Host-only.
+std::vector<int> partition_groups(const ttn_s* ref, int parts, std::vector<int>* cuts_out);
 
 }  // namespace tcbc

@@ -1,0 +1,148 @@
+"""Multi-GPU subtree partition (SURVEY §8(e) mechanism 2; include/ttn_cbc.h ttn_ctx_set_comm).
+
+CPU (host logic, no device): the partition plan covers the tree with whole subtrees under a
+connected replicated top, and two gloo ranks agree on the plan, on the NCCL-id transport and
+on a disjoint, complete split of the subtree work.  GPU: the partitioned schedule (1-rank
+NCCL communicator, 2 and 4 subtree groups) reproduces the plain apply.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+TREES = {
+    "cfg4_t3ns": W.make_config(4).parent,
+    "binary31": W.complete_binary(31),
+    "binary63": W.complete_binary(63),
+    "star3x2": W.star_of_chains_literal(3, 2),
+    "chain9": W.chain(9),
+}
+
+
+def _plan(parent, parts):
+    import paper_2601_19650_b200 as P
+    return P.ttn_partition_plan(parent, parts)
+
+
+@pytest.mark.parametrize("name", sorted(TREES))
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_plan_is_whole_subtrees_under_connected_top(name, parts):
+    parent = TREES[name]
+    g = _plan(parent, parts)
+    n = len(parent)
+    root = parent.index(-1)
+    assert g[root] == -1
+    for i in range(n):
+        p = parent[i]
+        if p < 0:
+            continue
+        if g[i] == -1:
+            assert g[p] == -1, "the top must be connected to the root"
+        elif g[p] != -1:
+            assert g[p] == g[i], "a subtree lies in one group"
+    assert all(-1 <= x < max(parts, 1) for x in g)
+    if parts == 1:
+        assert all(x == -1 for x in g)
+
+
+def test_plan_config4_uses_the_chains():
+    parent = TREES["cfg4_t3ns"]
+    g2, g4 = _plan(parent, 2), _plan(parent, 4)
+    assert g2.count(-1) == 1 and sorted(g2.count(k) for k in range(2)) == [33, 33]   # junction subtrees
+    assert g4.count(-1) == 3 and [g4.count(k) for k in range(4)] == [16, 16, 16, 16]  # the 4 chains (B:10)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2601_19650_b200 as P
+        fake_id = bytes(np.random.default_rng(1234).integers(0, 256, 128, dtype=np.uint8)) if rank == 0 else None
+        uid = P.share_bytes(fake_id, 128)
+        parent = TREES["cfg4_t3ns"]
+        plan = P.ttn_partition_plan(parent, 4)
+        mine = [i for i, x in enumerate(plan) if x >= 0 and x % world == rank]
+        out[rank] = (uid, plan, mine)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_gloo_ranks_agree_on_id_plan_and_split():
+    import torch.multiprocessing as mp
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gloo_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    (u0, p0, m0), (u1, p1, m1) = out[0], out[1]
+    assert u0 == u1 and len(u0) == 128
+    assert p0 == p1
+    assert not set(m0) & set(m1)
+    assert sorted(m0 + m1) == [i for i, x in enumerate(p0) if x >= 0]
+    assert len(m0) == len(m1) == 32
+
+
+# ------------------------------------------------------------------------------ GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("tree,chi,D,mb", [("binary31", 4, 3, 6), ("star3x2", 3, 2, 4), ("binary63", 3, 2, 4)])
+@pytest.mark.parametrize("parts", [2, 4])
+def test_partitioned_schedule_matches_plain_apply(tree, chi, D, mb, parts):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_19650_b200 as P
+    from ._helpers import gpu_pair, to_oracle, distances
+    from oracle import norm
+    parent = TREES[tree]
+    inst = W.configs.random_instance(parent, [2] * len(parent), chi, D, mb, seed=5)
+    ctx = P.Context(0)
+    try:
+        op, st = gpu_pair(P, ctx, inst)
+        ref, rep0 = P.cbc_apply(ctx, op, st, mb)
+        P.ttn_ctx_set_comm(ctx, P.ttn_comm_unique_id(), 0, 1, parts)
+        got, rep1 = P.cbc_apply(ctx, op, st, mb)
+        P.ttn_ctx_set_comm(ctx, None)
+        a, b = to_oracle(P, got, parent), to_oracle(P, ref, parent)
+        assert a.bonds() == b.bonds()
+        d_cos, d_rel = distances(a, b)
+        assert d_rel <= 1e-12, (d_cos, d_rel)
+        assert abs(rep1["discarded_weight_sum"] - rep0["discarded_weight_sum"]) <= 1e-12 * max(1.0, rep0["discarded_weight_sum"])
+        assert abs(rep1["norm"] - rep0["norm"]) <= 1e-12 * rep0["norm"]
+    finally:
+        ctx.close()
+
+
+@pytest.mark.gpu
+def test_partitioned_config4_matches_golden():
+    import json
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_19650_b200 as P
+    from ._helpers import gpu_pair, to_oracle
+    from oracle import norm
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg4_seed0.json")))
+    inst = W.make_config(4, seed=0)
+    ctx = P.Context(0)
+    try:
+        op, st = gpu_pair(P, ctx, inst)
+        P.ttn_ctx_set_comm(ctx, P.ttn_comm_unique_id(), 0, 1, 4)
+        out, rep = P.cbc_apply(ctx, op, st, inst.max_bond)
+        P.ttn_ctx_set_comm(ctx, None)
+        phi = to_oracle(P, out, inst.parent)
+        assert phi.bonds() == gold["bonds"]
+        assert abs(norm(phi) ** 2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"]
+    finally:
+        ctx.close()
