@@ -89,7 +89,12 @@ TTN_API const char* ttn_version(void);
  *            legs.  MPS / MPO: parent[i] = i-1, site i's tensor is [d, a_left, a_right]
  *            (Eq. 3).
  *  data_on_device  0: data[i] are host pointers (copied H2D); 1: device pointers (D2D).
- * The data is copied; the caller keeps ownership of its buffers.
+ * The data is copied; the caller keeps ownership of its buffers.  Consecutive nodes whose
+ * tensors are adjacent in memory (one packed buffer, node 0 first) are copied in one
+ * transfer.  Pageable host data is fully copied when the call returns; page-locked
+ * (pinned) host data and device data are copied asynchronously on the ctx stream, so the
+ * caller must not modify them until the stream has passed the copy (every call that
+ * returns host values, e.g. cbc_apply, synchronises it).
  * Errors: TOPOLOGY (no single root, cycle), ARG (NULL, d < 1, bond < 1).               */
 TTN_API ttn_status ttn_create(ttn_ctx ctx, ttn_kind kind, int32_t n_nodes, const int32_t* parent,
                       const int32_t* phys_dim, const int64_t* bond,

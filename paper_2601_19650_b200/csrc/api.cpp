@@ -116,13 +116,31 @@ ttn_status ttn_create(ttn_ctx ctx, ttn_kind kind, int32_t n_nodes, const int32_t
     finalize_shapes(t);
     TTN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t->data), sizeof(cplx) * std::max<int64_t>(t->total, 1),
                              ctx->stream));
-    for (int i = 0; i < n_nodes; ++i) {
-      int64_t e = 1;
-      for (auto x : t->shape[i]) e *= x;
-      TTN_CUDA(cudaMemcpyAsync(t->node(i), data[i], sizeof(cplx) * e,
-                               data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    // runs of nodes whose source tensors are adjacent in memory (a packed TTN buffer) move
+    // with one copy each
+    const cudaMemcpyKind kind_cp = data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    bool pinned = !data_on_device;
+    for (int i = 0; i < n_nodes;) {
+      int j = i + 1;
+      int64_t run = 0;
+      for (auto x : t->shape[i]) run = (run ? run : 1) * x;
+      while (j < n_nodes && data[j] == data[i] + run) {
+        int64_t e = 1;
+        for (auto x : t->shape[j]) e *= x;
+        run += e;
+        ++j;
+      }
+      if (pinned) {
+        cudaPointerAttributes at;
+        pinned = cudaPointerGetAttributes(&at, data[i]) == cudaSuccess && at.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+      }
+      TTN_CUDA(cudaMemcpyAsync(t->node(i), data[i], sizeof(cplx) * run, kind_cp, ctx->stream));
+      i = j;
     }
-    if (!data_on_device) ctx->sync();   // host buffers may be pageable: finish before returning
+    // pageable host buffers: finish before returning; pinned ones stay stream-ordered (the
+    // caller keeps them unchanged until the ctx stream has passed the copy)
+    if (!data_on_device && !pinned) ctx->sync();
   });
   if (s != TTN_OK) {
     if (t) {
