@@ -207,26 +207,42 @@ PlanT make_plan(const Task& t) {
   return P;
 }
 
-std::string plan_key(const Task& t) {
-  std::ostringstream os;
-  for (auto& o : t.ops) {
-    os << (o.conj ? 'c' : 'n');
-    for (size_t i = 0; i < o.labels.size(); ++i) os << o.labels[i] << ':' << o.dims[i] << ',';
-    os << '|';
+// plan key: the integer signature of the task (per operand: conj flag, labels, extents;
+// then the output labels), hashed without building strings (this lookup runs for every node
+// of every instance at every level: ~1e5 times per config-5 step)
+struct KeyHash {
+  size_t operator()(const std::vector<int64_t>& v) const {
+    uint64_t h = 1469598103934665603ull;
+    for (int64_t x : v) {
+      h ^= (uint64_t)x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+      h *= 1099511628211ull;
+    }
+    return (size_t)h;
   }
-  os << '>';
-  for (int l : t.out_labels) os << l << ',';
-  return os.str();
+};
+
+void plan_key(const Task& t, std::vector<int64_t>& k) {
+  k.clear();
+  for (auto& o : t.ops) {
+    k.push_back(o.conj ? -2 : -3);
+    for (size_t i = 0; i < o.labels.size(); ++i) {
+      k.push_back(o.labels[i]);
+      k.push_back(o.dims[i]);
+    }
+  }
+  k.push_back(-4);
+  for (int l : t.out_labels) k.push_back(l);
 }
 
 std::mutex g_plan_mu;
-std::unordered_map<std::string, PlanT>& plan_cache() {
-  static std::unordered_map<std::string, PlanT> c;
+std::unordered_map<std::vector<int64_t>, PlanT, KeyHash>& plan_cache() {
+  static std::unordered_map<std::vector<int64_t>, PlanT, KeyHash> c;
   return c;
 }
 
 const PlanT& get_plan(const Task& t) {
-  const std::string key = plan_key(t);
+  thread_local std::vector<int64_t> key;
+  plan_key(t, key);
   std::lock_guard<std::mutex> lk(g_plan_mu);
   auto& c = plan_cache();
   auto it = c.find(key);
@@ -308,14 +324,18 @@ void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st) {
   for (size_t i = 0; i < tasks.size(); ++i) {
     Task& t = tasks[i];
     plans[i] = &get_plan(t);
-    std::map<int, int64_t> dim;
-    for (auto& o : t.ops)
-      for (size_t j = 0; j < o.labels.size(); ++j) dim[o.labels[j]] = o.dims[j];
     t.out_dims.clear();
     int64_t tot = 1;
-    for (int l : t.out_labels) {
-      t.out_dims.push_back(dim.at(l));
-      tot *= dim.at(l);
+    for (int l : t.out_labels) {   // extent of each output label (first operand carrying it)
+      int64_t e = -1;
+      for (auto& o : t.ops) {
+        for (size_t j = 0; j < o.labels.size(); ++j)
+          if (o.labels[j] == l) { e = o.dims[j]; break; }
+        if (e >= 0) break;
+      }
+      if (e < 0) throw Error(TTN_ERR_ARG, "output label not carried by any operand");
+      t.out_dims.push_back(e);
+      tot *= e;
     }
     if (!t.out) t.out = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * std::max<int64_t>(tot, 1)));
     st.peak_entries = std::max(st.peak_entries, std::max(tot, plans[i]->peak));

@@ -1010,131 +1010,130 @@ __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
 // cluster are computed one after the other, each inverse-iteration step orthogonalised
 // (MGS) against the cluster's previous vectors, so degenerate spectra (e.g. isometric
 // inputs whose Gram is the identity) still give an orthonormal basis of the subspace.
+// K3b: clusters of close eigenvalues (gap <= 1e-5 ||T||; circuit Grams have exactly
+// degenerate ones).  One CTA per matrix walks its clusters; within a cluster every vector gets
+// its own thread (its own shifted dgttrf / dgttrs, as K3a), and after each solve the whole
+// block is re-orthonormalised by modified Gram-Schmidt over all threads -- block inverse
+// iteration, so the O(n) tridiagonal solves of a cluster run in parallel instead of one
+// after another.
 __global__ void __launch_bounds__(HEEV_THREADS) heev_invit_cluster(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
-  const int n = P.n, kmax = P.kmax, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = P.n, kmax = P.kmax, tid = threadIdx.x;
   const int k = P.k_out ? *P.k_out : kmax;
   const double* sd = P.work;
   const double* evec = P.work + n;
   const double tnorm = P.work[2 * n + S_TNORM];
   if (!(tnorm > 0.0)) return;
   double* Z = P.work + 2 * n + 8;
+  const size_t NK = (size_t)n * kmax;
+  double* DL = Z + NK;
+  double* Dg = DL + NK;
+  double* DU = Dg + NK;
+  double* DU2 = DU + NK;
+  double* PV = DU2 + NK;
   const double* cst = cluster_arrays(P);
   const double* csz = cst + kmax;
-  double* scr = const_cast<double*>(csz) + kmax + (size_t)warp * 6 * n;
-  double* DL = scr;
-  double* Dg = scr + n;
-  double* DU = scr + 2 * n;
-  double* DU2 = scr + 3 * n;
-  double* PV = scr + 4 * n;
-  double* y = scr + 5 * n;
   const double pert = DBL_EPSILON * tnorm;
-  int ci = 0;
+  __shared__ double2 red[HEEV_WARPS + 1];
+  __shared__ double s_scale[256];
+#define AT(arr, i, t) arr[(size_t)(i) * kmax + (t)]
   for (int t0 = 0; t0 < k; ++t0) {
     if ((int)cst[t0] != t0 || csz[t0] < 2.0) continue;   // not the start of a multi-vector cluster
-    if ((ci++ % HEEV_WARPS) != warp) continue;
-    const int t1 = t0 + (int)csz[t0];
-    for (int t = t0; t < t1; ++t) {
-      double lam = P.lam[t];
-      if (t > t0) lam = fmin(lam, P.lam[t - 1] - 10.0 * DBL_EPSILON * tnorm);   // keep shifts apart (dstein)
-      if (lane == 0) {   // dgttrf of T - lam I
-        double d_i = sd[0] - lam, du_i = n > 1 ? evec[0] : 0.0;
-        for (int i = 0; i < n - 1; ++i) {
-          const double dl = evec[i];
-          double d_n = sd[i + 1] - lam, du_n = (i < n - 2) ? evec[i + 1] : 0.0, du2 = 0.0, l, p = 0.0;
-          if (fabs(d_i) >= fabs(dl)) {
-            if (fabs(d_i) < pert) d_i = copysign(pert, d_i == 0.0 ? 1.0 : d_i);
-            l = dl / d_i;
-            d_n -= l * du_i;
-          } else {
-            l = d_i / dl;
-            const double old_du = du_i;
-            d_i = dl;
-            du_i = d_n;
-            du2 = du_n;
-            d_n = old_du - l * d_n;
-            du_n = -l * du_n;
-            p = 1.0;
-          }
+    const int t1 = t0 + (int)csz[t0], c = t1 - t0;
+    // ---- factor T - lam_t I for every member (thread per vector), random start vectors
+    for (int t = t0 + tid; t < t1; t += HEEV_THREADS) {
+      const double lam = P.lam[t] - (t - t0) * 10.0 * DBL_EPSILON * tnorm;   // shifts kept apart (dstein)
+      double d_i = sd[0] - lam, du_i = n > 1 ? evec[0] : 0.0;
+      for (int i = 0; i < n - 1; ++i) {
+        const double dl = evec[i];
+        double d_n = sd[i + 1] - lam, du_n = (i < n - 2) ? evec[i + 1] : 0.0, du2 = 0.0, l, p = 0.0;
+        if (fabs(d_i) >= fabs(dl)) {
           if (fabs(d_i) < pert) d_i = copysign(pert, d_i == 0.0 ? 1.0 : d_i);
-          Dg[i] = 1.0 / d_i;
-          DU[i] = du_i;
-          DU2[i] = du2;
-          DL[i] = l;
-          PV[i] = p;
-          d_i = d_n;
-          du_i = du_n;
+          l = dl / d_i;
+          d_n -= l * du_i;
+        } else {
+          l = d_i / dl;
+          const double old_du = du_i;
+          d_i = dl;
+          du_i = d_n;
+          du2 = du_n;
+          d_n = old_du - l * d_n;
+          du_n = -l * du_n;
+          p = 1.0;
         }
         if (fabs(d_i) < pert) d_i = copysign(pert, d_i == 0.0 ? 1.0 : d_i);
-        Dg[n - 1] = 1.0 / d_i;
+        AT(Dg, i, t) = 1.0 / d_i;
+        AT(DU, i, t) = du_i;
+        AT(DU2, i, t) = du2;
+        AT(DL, i, t) = l;
+        AT(PV, i, t) = p;
+        d_i = d_n;
+        du_i = du_n;
       }
-      for (int i = lane; i < n; i += 32)
-        y[i] = (double)(hash32((unsigned)(t * 7919 + i * 104729 + 12345)) & 0xffffff) / 16777216.0 - 0.5;
-      __syncwarp();
-      for (int it = 0; it < 4; ++it) {
-        if (lane == 0) {   // dgttrs with overflow rescaling
-          double cur = y[0];
-          for (int i = 0; i < n - 1; ++i) {
-            const double nxt = y[i + 1];
-            if (PV[i] == 0.0) { y[i] = cur; cur = nxt - DL[i] * cur; }
-            else { y[i] = nxt; cur = cur - DL[i] * nxt; }
-          }
-          double y2 = 0.0, y1 = cur * Dg[n - 1];
-          y[n - 1] = y1;
-          for (int i = n - 2; i >= 0; --i) {
-            double yi = (y[i] - DU[i] * y1 - DU2[i] * y2) * Dg[i];
-            if (fabs(yi) > 1e100) {
-              for (int q = 0; q < n; ++q) if (q != i) y[q] *= 1e-100;
-              yi *= 1e-100; y1 *= 1e-100; y2 *= 1e-100;
-            }
-            y[i] = yi;
-            y2 = y1;
-            y1 = yi;
-          }
-        }
-        __syncwarp();
-        double mx = 0.0;
-        for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(y[i]));
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
-        for (int i = lane; i < n; i += 32) y[i] *= inv;
-        __syncwarp();
-        for (int rep = 0; rep < 2; ++rep)
-          for (int q = t0; q < t; ++q) {   // MGS against the cluster's previous vectors
-            double dt = 0.0;
-            for (int i = lane; i < n; i += 32) dt += y[i] * Z[(size_t)i * kmax + q];
-            dt = warp_sum(dt);
-            for (int i = lane; i < n; i += 32) y[i] -= dt * Z[(size_t)i * kmax + q];
-            __syncwarp();
-          }
-        double nr = 0.0;
-        for (int i = lane; i < n; i += 32) nr += y[i] * y[i];
-        nr = warp_sum(nr);
-        if (!(nr > 1e-200)) {   // collapsed onto the previous vectors: restart from a new direction
-          for (int i = lane; i < n; i += 32)
-            y[i] = (double)(hash32((unsigned)(t * 31 + i * 7877 + it * 131071 + 99)) & 0xffffff) / 16777216.0 - 0.5;
-          __syncwarp();
-          continue;
-        }
-        const double s = 1.0 / sqrt(nr);
-        for (int i = lane; i < n; i += 32) y[i] *= s;
-        __syncwarp();
-      }
-      for (int q = t0; q < t; ++q) {   // final projection + normalisation
-        double dt = 0.0;
-        for (int i = lane; i < n; i += 32) dt += y[i] * Z[(size_t)i * kmax + q];
-        dt = warp_sum(dt);
-        for (int i = lane; i < n; i += 32) y[i] -= dt * Z[(size_t)i * kmax + q];
-        __syncwarp();
-      }
-      double nr = 0.0;
-      for (int i = lane; i < n; i += 32) nr += y[i] * y[i];
-      nr = warp_sum(nr);
-      const double s = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
-      for (int i = lane; i < n; i += 32) Z[(size_t)i * kmax + t] = y[i] * s;
-      __syncwarp();
+      if (fabs(d_i) < pert) d_i = copysign(pert, d_i == 0.0 ? 1.0 : d_i);
+      AT(Dg, n - 1, t) = 1.0 / d_i;
+      for (int i = 0; i < n; ++i)
+        AT(Z, i, t) = (double)(hash32((unsigned)(t * 7919 + i * 104729 + 12345)) & 0xffffff) / 16777216.0 - 0.5;
     }
+    __syncthreads();
+    for (int it = 0; it < 3; ++it) {
+      // ---- solve (T - lam_t I) y = z in place (dgttrs), rescaled to max |y| = 1
+      for (int t = t0 + tid; t < t1; t += HEEV_THREADS) {
+        double cur = AT(Z, 0, t);
+        for (int i = 0; i < n - 1; ++i) {
+          const double nxt = AT(Z, i + 1, t);
+          const double l = AT(DL, i, t);
+          if (AT(PV, i, t) == 0.0) { AT(Z, i, t) = cur; cur = nxt - l * cur; }
+          else { AT(Z, i, t) = nxt; cur = cur - l * nxt; }
+        }
+        double y2 = 0.0, y1 = cur * AT(Dg, n - 1, t);
+        AT(Z, n - 1, t) = y1;
+        double mx = fabs(y1);
+        for (int i = n - 2; i >= 0; --i) {
+          double yi = (AT(Z, i, t) - AT(DU, i, t) * y1 - AT(DU2, i, t) * y2) * AT(Dg, i, t);
+          if (fabs(yi) > 1e100) {
+            const double f = 1e-100;
+            for (int q = i + 1; q < n; ++q) AT(Z, q, t) *= f;
+            yi *= f; y1 *= f; y2 *= f; mx *= f;
+          }
+          AT(Z, i, t) = yi;
+          mx = fmax(mx, fabs(yi));
+          y2 = y1;
+          y1 = yi;
+        }
+        const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
+        for (int i = 0; i < n; ++i) AT(Z, i, t) *= sc;
+      }
+      __syncthreads();
+      // ---- modified Gram-Schmidt over the block (twice is enough for exact degeneracy)
+      for (int rep = 0; rep < 2; ++rep)
+        for (int j = t0; j < t1; ++j) {
+          double part = 0.0;
+          for (int i = tid; i < n; i += HEEV_THREADS) part += AT(Z, i, j) * AT(Z, i, j);
+          const double nr = block_sum2(part, 0.0, red).x;
+          const double inv = nr > 1e-300 ? 1.0 / sqrt(nr) : 0.0;
+          for (int i = tid; i < n; i += HEEV_THREADS) AT(Z, i, j) *= inv;
+          __syncthreads();
+          if (j + 1 >= t1) break;
+          // projections of the later vectors onto j: warp per vector
+          const int lane = tid & 31, warp = tid >> 5;
+          for (int q = j + 1 + warp; q < t1; q += HEEV_WARPS) {
+            double d = 0.0;
+            for (int i = lane; i < n; i += 32) d += AT(Z, i, j) * AT(Z, i, q);
+            d = warp_sum(d);
+            if (lane == 0) s_scale[(q - j - 1) & 255] = d;
+          }
+          __syncthreads();
+          for (int e = tid; e < n * (t1 - j - 1); e += HEEV_THREADS) {
+            const int q = j + 1 + e / n, i = e % n;
+            if (q - j - 1 < 256) AT(Z, i, q) -= s_scale[q - j - 1] * AT(Z, i, j);
+          }
+          __syncthreads();
+        }
+    }
+    (void)c;
   }
+#undef AT
 }
 
 }  // namespace
