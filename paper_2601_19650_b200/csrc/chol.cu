@@ -26,6 +26,13 @@ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
 }
 
+// one DMMA (mma.sync m8n8k4 f64): {c0, c1} += a (8x4 row) * b (4x8 col), one element per lane
+__device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
 __device__ double block_max(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -44,12 +51,12 @@ __device__ double block_max(double v, double* red) {
 constexpr int CH_NB = 16;      // panel / row-block width
 constexpr int CH_THREADS = 512;
 
-// Blocked right-looking Cholesky (lower): for each 16-column panel, (1) the panel is staged in
-// shared memory, (2) its 16 x 16 diagonal block is factored by one warp (lane = row),
-// (3) the rows below are solved against L11^H (thread per row), (4) the panel is written back
-// and the trailing lower triangle is updated once per panel (A22 -= P P^H) with 4 x 4 register
-// tiles reading the staged panel (16 complex MACs per element per panel instead of one
-// global read-modify-write per column).  One CTA per matrix.
+// Blocked right-looking Cholesky (lower; B:5 (b)): for each 16-column panel, (1) the panel is
+// staged in shared memory, (2) its 16 x 16 diagonal block is factored by one warp (lane =
+// row), (3) the rows below are solved against L11^H (thread per row), (4) the panel is written
+// back and the trailing lower triangle is updated once per panel (A22 -= P P^H) on the FP64
+// tensor cores (DMMA), reading the staged panel (one global read-modify-write per element per
+// panel instead of per column).  One CTA per matrix.
 __global__ void __launch_bounds__(CH_THREADS) potrf_grouped(const PotrfProblem* __restrict__ probs) {
   const PotrfProblem P = probs[blockIdx.x];
   const int n = P.n;
@@ -127,47 +134,40 @@ __global__ void __launch_bounds__(CH_THREADS) potrf_grouped(const PotrfProblem* 
       const int r = e / jb, c = e % jb;
       if (c <= r) A[(long long)(j0 + r) * ld + j0 + c] = Pn[r * CH_NB + c];
     }
-    // trailing update on 4x4 tiles of the lower triangle of rows/cols [jb, rows)
-    const int t = rows - jb, tb = (t + 3) / 4;
+    // trailing update A22 -= P P^H on the FP64 tensor path: warp per 8x8 tile of the lower
+    // triangle, 4 k-steps of DMMA m8n8k4 per complex product (4M rule), both operand
+    // fragments read straight from the staged panel (B = conj(P)^T uses the same index map)
+    const int t = rows - jb, tb = (t + 7) / 8;
     const int ntiles = tb * (tb + 1) / 2;
-    for (int e = tid; e < ntiles; e += CH_THREADS) {
+    const int fr = lane >> 2, fc = lane & 3;
+    for (int e = warp; e < ntiles; e += CH_THREADS / 32) {
       int bi = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
       while (bi * (bi + 1) / 2 > e) --bi;
       while ((bi + 1) * (bi + 2) / 2 <= e) ++bi;
       const int bj = e - bi * (bi + 1) / 2;
-      const int r0 = jb + 4 * bi, l0 = jb + 4 * bj;
-      cplx acc[4][4];
+      const int r0 = jb + 8 * bi, l0 = jb + 8 * bj;
+      double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
-      for (int c = 0; c < jb; ++c) {
-        cplx pr[4], pl[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          pr[a] = (r0 + a < rows) ? Pn[(r0 + a) * CH_NB + c] : make_double2(0.0, 0.0);
-          pl[a] = (l0 + a < rows) ? Pn[(l0 + a) * CH_NB + c] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const cplx u = cmulc(pr[a], pl[b]);
-            acc[a][b].x += u.x;
-            acc[a][b].y += u.y;
-          }
+      for (int q = 0; q < CH_NB / 4; ++q) {
+        const int k = q * 4 + fc;
+        const cplx a = (r0 + fr < rows && k < jb) ? Pn[(r0 + fr) * CH_NB + k] : make_double2(0.0, 0.0);
+        const cplx bb = (l0 + fr < rows && k < jb) ? Pn[(l0 + fr) * CH_NB + k] : make_double2(0.0, 0.0);
+        const double br = bb.x, bim = -bb.y;   // B = conj(P_l)^T
+        dmma8(cr0, cr1, a.x, br);
+        dmma8(ci0, ci1, a.x, bim);
+        dmma8(cr0, cr1, -a.y, bim);
+        dmma8(ci0, ci1, a.y, br);
       }
+      const int r = r0 + fr;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int r = r0 + a, l = l0 + b;
-          if (r < rows && l <= r) {
-            cplx* p = A + (long long)(j0 + r) * ld + j0 + l;
-            p->x -= acc[a][b].x;
-            p->y -= acc[a][b].y;
-          }
+      for (int h = 0; h < 2; ++h) {
+        const int l = l0 + 2 * fc + h;
+        if (r < rows && l <= r) {
+          cplx* p = A + (long long)(j0 + r) * ld + j0 + l;
+          p->x -= h ? cr1 : cr0;
+          p->y -= h ? ci1 : ci0;
         }
+      }
     }
     __syncthreads();
   }

@@ -1,0 +1,102 @@
+"""GPU edge cases of the CBC path vs the CPU oracle (same seeded inputs): single-node and
+two-node trees, max_bond = 1, ragged per-edge bonds, a root that is not node 0, physical
+dimension 1, and a batch whose instances have different bonds (cbc_apply_batch allows it)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import TTN, cbc_apply as oracle_cbc, exact_apply, norm, to_dense_operator, to_dense_state
+from workloads.configs import Instance
+from workloads.generators import operator_shapes, random_tree_tensors, state_shapes
+
+from ._helpers import distances, gpu_pair, oracle_pair, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_19650_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def ragged_instance(parent, phys, sbond, obond, max_bond, seed):
+    rng = np.random.default_rng(seed)
+    st = random_tree_tensors(rng, state_shapes(parent, phys, sbond))
+    op = random_tree_tensors(rng, operator_shapes(parent, phys, obond))
+    return Instance("ragged", list(parent), list(phys), list(sbond), list(obond), st, op, max_bond)
+
+
+def run_and_check(P, ctx, inst, exact=False):
+    op_g, st_g = gpu_pair(P, ctx, inst)
+    out, rep = P.cbc_apply(ctx, op_g, st_g, inst.max_bond)
+    phi_g = to_oracle(P, out, inst.parent)
+    op_o, psi_o = oracle_pair(inst)
+    phi_o = oracle_cbc(op_o, psi_o, inst.max_bond)
+    assert phi_g.bonds() == phi_o.bonds()
+    d_cos, d_rel = distances(phi_g, phi_o)
+    assert d_cos <= 1e-10, (d_cos, d_rel)
+    on2 = norm(exact_apply(op_o, psi_o)) ** 2
+    assert abs(norm(phi_g) ** 2 - norm(phi_o) ** 2) <= 1e-10 * on2
+    if exact:
+        ex = to_dense_operator(op_o) @ to_dense_state(psi_o)
+        assert np.linalg.norm(to_dense_state(phi_g) - ex) <= 1e-12 * np.linalg.norm(ex)
+    return phi_g, rep
+
+
+def test_single_node_tree(P, ctx):
+    inst = ragged_instance([-1], [5], [1], [1], 4, seed=1)
+    phi, rep = run_and_check(P, ctx, inst, exact=True)   # no bond to compress: phi = O psi
+    assert phi.bonds() == [1]
+
+
+def test_two_node_tree(P, ctx):
+    for mb in (1, 2, 64):
+        inst = ragged_instance([-1, 0], [3, 4], [1, 5], [1, 3], mb, seed=2)
+        run_and_check(P, ctx, inst, exact=(mb == 64))
+
+
+def test_max_bond_one(P, ctx):
+    inst = W.configs.random_instance(W.complete_binary(7), [2] * 7, 3, 2, 1, seed=3)
+    phi, rep = run_and_check(P, ctx, inst)
+    assert phi.bonds() == [1] * 7
+
+
+def test_ragged_bonds_and_root_in_the_middle(P, ctx):
+    # chain 0-1-2-3-4-5 rooted at node 3 (parent array is not heap-ordered)
+    parent = [1, 2, 3, -1, 3, 4]
+    sb = [3, 5, 7, 1, 6, 2]
+    ob = [2, 3, 2, 1, 4, 3]
+    for mb in (64, 5):
+        inst = ragged_instance(parent, [2, 3, 2, 2, 3, 2], sb, ob, mb, seed=4)
+        run_and_check(P, ctx, inst, exact=(mb == 64))
+
+
+def test_physical_dim_one_nodes(P, ctx):
+    parent = W.complete_binary(7)
+    inst = ragged_instance(parent, [1, 2, 1, 2, 2, 2, 2], [1, 4, 3, 2, 2, 3, 3], [1, 2, 3, 2, 2, 2, 2], 3, seed=5)
+    run_and_check(P, ctx, inst)
+
+
+def test_batch_with_different_bonds(P, ctx):
+    parent = W.complete_binary(15)
+    insts = [W.configs.random_instance(parent, [2] * 15, chi, D, 6, seed=10 + chi) for chi, D in ((3, 2), (5, 3), (4, 4))]
+    pairs = [gpu_pair(P, ctx, i) for i in insts]
+    outs, reps = P.cbc_apply_batch(ctx, [p[0] for p in pairs], [p[1] for p in pairs], 6)
+    for inst, out, rep in zip(insts, outs, reps):
+        phi_g = to_oracle(P, out, parent)
+        op_o, psi_o = oracle_pair(inst)
+        phi_o = oracle_cbc(op_o, psi_o, 6)
+        assert phi_g.bonds() == phi_o.bonds()
+        assert distances(phi_g, phi_o)[0] <= 1e-10
+        assert abs(rep["norm"] - norm(phi_o)) <= 1e-10 * norm(phi_o)

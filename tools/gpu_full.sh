@@ -1,11 +1,9 @@
 # one GPU call: parity tests, full bench line, ncu launch list + one full capture of the top kernel
-set -o pipefail
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -2 gpurun_out/bench.err
 Q="python bench.py --quick --steps 1 --warmup 1"
 timeout 300 $Q > gpurun_out/quick.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $Q > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:zgemm -s 40 -c 3 -o gpurun_out/prof_zgemm $Q > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:heev_tridiag -s 2 -c 1 -o gpurun_out/prof_heev $Q > gpurun_out/ncu_full_heev.log 2>&1; echo "ncu heev rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:zgemm -s 20 -c 6 -o gpurun_out/prof_zgemm $Q > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
