@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workers", type=int, default=None, help="concurrent sub-batches (ttn_ctx_set_workers)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="short run for ncu: no e2e/cpu/clocks")
     return ap.parse_args()
@@ -204,6 +205,9 @@ def run_native(args, rank, world, local_rank):
     ctx = P.Context(local_rank, stream.cuda_stream)
     if partitioned:
         P.comm_bootstrap(ctx, parts=4 if world <= 4 else world)
+    workers = args.workers if args.workers is not None else {5: 4}.get(cfg, 1)
+    if workers > 1 and not partitioned:
+        P.ttn_ctx_set_workers(ctx, workers)
     mb = insts[0].max_bond
     parent, phys = insts[0].parent, insts[0].phys
 
@@ -391,7 +395,7 @@ def run_native(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "c128 (f64)",
         "data": "synthetic",
-        "config": dict(workload_desc(cfg, batch),
+        "config": dict(workload_desc(cfg, batch), workers=workers,
                        parallelism=(f"subtree-partitioned x{world} (NCCL, {4 if world <= 4 else world} groups)" if partitioned
                                     else f"instance-sharded x{world}")),
         "fp64_tflops_end_to_end": flops_all / (ms_max / 1000.0) / 1e12,

@@ -135,6 +135,15 @@ TTN_API ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const
 TTN_API ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out);
 /* Batched overlaps <a_j|b_j>, j < n.                                                      */
 TTN_API ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b, ttn_c128* out);
+/* Split every later cbc_apply_batch of >= 2n instances on ctx into n concurrent sub-batches,
+ * each on an internal worker context (its own non-blocking stream, staging ring and arenas)
+ * driven by its own host thread; the worker streams wait for ctx's stream at the start and
+ * ctx's stream waits for them at the end, and the results belong to ctx.  Batches of small
+ * trees (config 5's circuit layers) are bound by host-side planning and the per-level rank
+ * synchronisations; overlapping sub-batches hides them.  n = 1 (default) turns it off.
+ * Not combined with ttn_ctx_set_comm (a partitioned apply runs on ctx itself).  Errors: ARG. */
+TTN_API ttn_status ttn_ctx_set_workers(ttn_ctx ctx, int n);
+
 /* ---------------------------------------------------------------- multi-GPU            */
 /* 128-byte NCCL unique id for a new communicator: create it on one rank and hand the same
  * bytes to every rank (e.g. by a torch.distributed broadcast).  NCCL is loaded at run time

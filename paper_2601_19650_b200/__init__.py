@@ -199,6 +199,11 @@ def ttn_norm(ctx: Context, a: TTN) -> float:
     return v.value
 
 
+def ttn_ctx_set_workers(ctx: Context, n: int) -> None:
+    """Concurrent sub-batches for cbc_apply_batch (include/ttn_cbc.h); n = 1 turns it off."""
+    L.check(ctx.h, L.load().ttn_ctx_set_workers(ctx.h, int(n)))
+
+
 # ---------------------------------------------------------------- multi-GPU (NCCL)
 def ttn_comm_unique_id() -> bytes:
     """128-byte NCCL unique id (create on one rank, share the bytes with the others)."""

@@ -5,7 +5,9 @@
 
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <new>
+#include <thread>
 #include <vector>
 
 using namespace tcbc;
@@ -81,11 +83,14 @@ ttn_status ttn_ctx_destroy(ttn_ctx ctx) {
   if (!ctx) return TTN_ERR_ARG;
   DeviceGuard g(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (auto* w : ctx->workers) ttn_ctx_destroy(w);
+  ctx->workers.clear();
   ctx->scratch.release();
   ctx->env.release();
   delete ctx->stager;
   delete ctx->comm;
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
+  if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TTN_OK;
 }
@@ -211,7 +216,46 @@ ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const ttn* st
   std::vector<ttn_s*> res(n, nullptr);
   ttn_status s = guard(ctx, [&] {
     std::vector<const ttn_s*> o(ops, ops + n), st(states, states + n);
-    cbc_apply_impl(ctx, n, o.data(), st.data(), max_bond, tol, res.data(), reps);
+    const int W = (int)ctx->workers.size();
+    if (W < 2 || ctx->comm || n < 2 * W) {
+      cbc_apply_impl(ctx, n, o.data(), st.data(), max_bond, tol, res.data(), reps);
+      return;
+    }
+    // W concurrent sub-batches, each on a worker context (own stream, staging ring, arenas)
+    // driven by its own host thread: one sub-batch's host-side planning and rank syncs
+    // overlap the others' kernels.  Streams are joined with events both ways.
+    cudaEvent_t start;
+    TTN_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    TTN_CUDA(cudaEventRecord(start, ctx->stream));
+    std::vector<std::exception_ptr> err(W);
+    std::vector<std::thread> th;
+    for (int w = 0; w < W; ++w) {
+      const int b0 = (int)((long long)n * w / W), b1 = (int)((long long)n * (w + 1) / W);
+      th.emplace_back([&, w, b0, b1] {
+        try {
+          ttn_ctx_s* wc = ctx->workers[w];
+          DeviceGuard gw(wc->device);
+          TTN_CUDA(cudaStreamWaitEvent(wc->stream, start, 0));
+          cbc_apply_impl(wc, b1 - b0, o.data() + b0, st.data() + b0, max_bond, tol, res.data() + b0,
+                         reps ? reps + b0 : nullptr);
+        } catch (...) {
+          err[w] = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int w = 0; w < W; ++w) {
+      cudaEvent_t done;
+      TTN_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      TTN_CUDA(cudaEventRecord(done, ctx->workers[w]->stream));
+      TTN_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
+      cudaEventDestroy(done);
+    }
+    cudaEventDestroy(start);
+    for (auto& r : res)
+      if (r) r->ctx = ctx;   // results belong to the caller's context from here on
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
   });
   if (s != TTN_OK) {
     for (auto* r : res) free_ttn(r);
@@ -234,6 +278,29 @@ ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b,
 }
 
 ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out) { return ttn_overlap_batch(ctx, 1, &a, &b, out); }
+
+ttn_status ttn_ctx_set_workers(ttn_ctx ctx, int n) {
+  if (!ctx || n < 1 || n > 64) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    cudaStreamSynchronize(ctx->stream);
+    for (auto* w : ctx->workers) ttn_ctx_destroy(w);
+    ctx->workers.clear();
+    if (n == 1) return;
+    for (int i = 0; i < n; ++i) {
+      cudaStream_t st;
+      TTN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      ttn_ctx w = nullptr;
+      ttn_status s = ttn_ctx_create(ctx->device, st, &w);
+      if (s != TTN_OK) {
+        cudaStreamDestroy(st);
+        throw Error(s, "worker context creation failed");
+      }
+      w->owns_stream = true;
+      ctx->workers.push_back(w);
+    }
+  });
+}
 
 ttn_status ttn_comm_unique_id(void* out128) {
   if (!out128) return TTN_ERR_ARG;

@@ -26,7 +26,6 @@ struct Profiler {
   std::vector<cudaEvent_t> pool;
   std::vector<Pending> pending;
   std::map<std::string, Acc> acc;
-  cudaEvent_t open = nullptr;
 
   cudaEvent_t get() {
     if (!pool.empty()) {
@@ -65,25 +64,27 @@ Profiler& P() {
   return p;
 }
 
+thread_local cudaEvent_t t_open = nullptr;   // per host thread (worker contexts run concurrently)
+
 }  // namespace
 
 void prof_begin(cudaStream_t s) {
   Profiler& p = P();
   if (!p.on) return;
   std::lock_guard<std::mutex> g(p.mu);
-  p.open = p.get();
-  cudaEventRecord(p.open, s);
+  t_open = p.get();
+  cudaEventRecord(t_open, s);
 }
 
 void prof_end(cudaStream_t s, const char* family, double flops, double bytes) {
   Profiler& p = P();
   if (!p.on) return;
   std::lock_guard<std::mutex> g(p.mu);
-  if (!p.open) return;
+  if (!t_open) return;
   cudaEvent_t b = p.get();
   cudaEventRecord(b, s);
-  p.pending.push_back(Pending{p.open, b, family, flops, bytes});
-  p.open = nullptr;
+  p.pending.push_back(Pending{t_open, b, family, flops, bytes});
+  t_open = nullptr;
   if (p.pending.size() > 4096) p.harvest();
 }
 

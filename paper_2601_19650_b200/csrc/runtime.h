@@ -74,6 +74,8 @@ struct ttn_ctx_s {
   size_t dbuf_size = 0;
   int host_syncs = 0;
   tcbc::Comm* comm = nullptr;   // multi-GPU apply (ttn_ctx_set_comm)
+  std::vector<ttn_ctx_s*> workers;   // concurrent sub-batches (ttn_ctx_set_workers); own streams
+  bool owns_stream = false;
   int parts = 1;                // subtree groups of a partitioned apply
   void sync();             // cudaStreamSynchronize + stager epoch
   void ensure_small(size_t bytes);

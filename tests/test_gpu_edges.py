@@ -100,3 +100,24 @@ def test_batch_with_different_bonds(P, ctx):
         assert phi_g.bonds() == phi_o.bonds()
         assert distances(phi_g, phi_o)[0] <= 1e-10
         assert abs(rep["norm"] - norm(phi_o)) <= 1e-10 * norm(phi_o)
+
+
+def test_worker_subbatches_match_single_stream(P, ctx):
+    """ttn_ctx_set_workers: concurrent sub-batches on internal streams give the same results."""
+    parent = W.complete_binary(15)
+    insts = [W.configs.random_instance(parent, [2] * 15, 4, 3, 6, seed=40 + s) for s in range(9)]
+    pairs = [gpu_pair(P, ctx, i) for i in insts]
+    ref, rref = P.cbc_apply_batch(ctx, [p[0] for p in pairs], [p[1] for p in pairs], 6)
+    P.ttn_ctx_set_workers(ctx, 4)
+    try:
+        got, rgot = P.cbc_apply_batch(ctx, [p[0] for p in pairs], [p[1] for p in pairs], 6)
+    finally:
+        P.ttn_ctx_set_workers(ctx, 1)
+    for a, b, ra, rb in zip(got, ref, rgot, rref):
+        x, y = to_oracle(P, a, parent), to_oracle(P, b, parent)
+        assert x.bonds() == y.bonds()
+        # same arithmetic per instance: the tensors agree to rounding (the overlap-based
+        # distance floors near 1e-8, reading A18, so compare entries)
+        for tx, ty in zip(x.tensors, y.tensors):
+            assert np.allclose(tx, ty, rtol=0, atol=1e-12 * max(1.0, np.abs(ty).max()))
+        assert abs(ra["norm"] - rb["norm"]) <= 1e-12 * rb["norm"]
