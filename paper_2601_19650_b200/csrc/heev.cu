@@ -575,6 +575,17 @@ __global__ void __launch_bounds__(CL_THREADS) heev_tridiag_cluster(const HeevPro
 }
 
 // ---------------------------------------------------------------- K2: eigenvalues
+// 1/b from the SFU seed and two Newton steps (~1 ulp; |b| >= pivmin > 0 here).  The Sturm
+// recurrence is bound by its FP64 divisions; the count is insensitive to ulp-level pivot
+// errors (an O(eps ||T||) perturbation of T, below the bisection tolerance atol = 4 eps ||T||).
+__device__ __forceinline__ double frcp(double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  r = r * fma(-b, r, 2.0);
+  r = r * fma(-b, r, 2.0);
+  return r;
+}
+
 // One warp per (matrix, eigenvalue): multisection.  Each lane evaluates Sturm counts at two
 // of 64 interior points of [lo, hi] (two interleaved chains hide the division latency); the
 // interval shrinks 65x per round, so ~9 rounds reach the dstebz tolerance instead of ~50
@@ -601,8 +612,8 @@ __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, in
     if (q2 <= pivmin) { ++c2; q2 = fmin(q2, -pivmin); }
     for (int i = 1; i < n; ++i) {
       const double di = d[i], ep = e[i - 1], ei = ep * ep;
-      q1 = di - x1 - ei / q1;
-      q2 = di - x2 - ei / q2;
+      q1 = di - x1 - ei * frcp(q1);
+      q2 = di - x2 - ei * frcp(q2);
       if (q1 <= pivmin) { ++c1; q1 = fmin(q1, -pivmin); }
       if (q2 <= pivmin) { ++c2; q2 = fmin(q2, -pivmin); }
     }
