@@ -181,6 +181,7 @@ struct Job {
   double *theta, *res, *dscale, *hwork, *thr;
   cplx* Vr;               // Ritz basis before the last filter pass (restored if that pass breaks down)
   double prev_worst = 1e300, prev_top = 0.0;
+  int c = 0;              // locked (converged) leading Ritz vectors: not filtered any more
   int* info;
   bool done = false;
 };
@@ -233,30 +234,51 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
     kern<<<dim3(296, (unsigned)L.size()), 256, 0, s>>>(d);
     count_launch();
   };
-  // orthonormalise V (n x p) of every active job in place: shifted CholeskyQR3 (Fukaya et al.):
-  // a first Cholesky pass of V^H V + s I (s ~ 1e-13 max diag) brings any block with
-  // cond <= ~1e13 to cond <= ~1e7, then CholeskyQR2 finishes; V keeps its span throughout.
+  // orthonormalise the unlocked tail V[:, c:p] of every active job in place: projected twice
+  // against the locked (already orthonormal) columns V[:, 0:c], then shifted CholeskyQR3
+  // (Fukaya et al.): a first Cholesky pass of Y^H Y + s I (s ~ 1e-13 max diag) brings any block
+  // with cond <= ~1e13 to cond <= ~1e7, then CholeskyQR2 finishes; the span is kept throughout.
   auto orth = [&](std::vector<Job*>& act) {
+    for (int rep = 0; rep < 2; ++rep) {   // Y -= V_L (V_L^H Y)
+      std::vector<GemmProblem> gp1, gp2;
+      for (Job* jp : act) {
+        Job& j = *jp;
+        if (j.c == 0) continue;
+        const int64_t n = j.n, p = j.p, c = j.c, w = p - c;
+        gp1.push_back(mk_gemm(j.V, OP_C, p, j.V + c, OP_N, p, j.Wg, w, c, w, n));
+        GemmProblem g2 = mk_gemm(j.V, OP_N, p, j.Wg, OP_N, w, j.V + c, p, n, w, c);
+        g2.alpha = make_double2(-1.0, 0.0);
+        g2.beta = make_double2(1.0, 0.0);
+        gp2.push_back(g2);
+      }
+      gemm_batch(ctx, gp1, st);
+      gemm_batch(ctx, gp2, st);
+    }
     for (int pass = 0; pass < 3; ++pass) {
       std::vector<GemmProblem> g1, g2;
       std::vector<PotrfProblem> p1;
       std::vector<TrtriProblem> t1;
       for (Job* jp : act) {
         Job& j = *jp;
-        const int64_t n = j.n, p = j.p;
-        g1.push_back(mk_gemm(j.V, OP_C, p, j.V, OP_N, p, j.Wg, p, p, p, n));
+        const int64_t n = j.n, p = j.p, c = j.c, w = p - c;
+        g1.push_back(mk_gemm(j.V + c, OP_C, p, j.V + c, OP_N, p, j.Wg, w, w, w, n));
         g1.back().sym = 1;
-        PotrfProblem pp{j.Wg, p, (int)p, 0, j.info + (pass == 2 ? 1 : 0), 1e-15};
+        PotrfProblem pp{j.Wg, w, (int)w, 0, j.info + (pass == 2 ? 1 : 0), 1e-15};
         pp.shift_rel = pass == 0 ? 1e-13 : 0.0;
         p1.push_back(pp);
-        t1.push_back(TrtriProblem{j.Wg, j.Li, p, (int)p, 0});
-        g2.push_back(mk_gemm(j.V, OP_N, p, j.Li, OP_C, p, j.Q1, p, n, p, p));
+        t1.push_back(TrtriProblem{j.Wg, j.Li, w, (int)w, 0});
+        g2.push_back(mk_gemm(j.V + c, OP_N, p, j.Li, OP_C, w, j.Q1 + c, p, n, w, w));
       }
       gemm_batch(ctx, g1, st);
       launch_potrf(p1.data(), (int)p1.size(), *ctx->stager, s);
       launch_trtri(t1.data(), (int)t1.size(), *ctx->stager, s);
       gemm_batch(ctx, g2, st);
-      for (Job* jp : act) std::swap(jp->V, jp->Q1);
+      for (Job* jp : act) {
+        Job& j = *jp;
+        const size_t w = (size_t)(j.p - j.c);
+        TTN_CUDA(cudaMemcpy2DAsync(j.V + j.c, sizeof(cplx) * j.p, j.Q1 + j.c, sizeof(cplx) * j.p, sizeof(cplx) * w,
+                                   (size_t)j.n, cudaMemcpyDeviceToDevice, s));
+      }
     }
   };
   // Rayleigh-Ritz of every active job: theta, V <- V Z (W <- G V Z), residuals of wanted pairs
@@ -325,8 +347,8 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
       if (dbgi) {
         double wr = 0.0;
         for (int t = 0; t < j.kmax; ++t) wr = std::max(wr, rs[t]);
-        fprintf(stderr, "[chfsi] iter %d job %d: theta0=%.6e theta_k=%.6e theta_p=%.6e maxres/theta0=%.3e info=%d,%d\n", iter, b,
-                th[0], th[j.kmax - 1], th[j.p - 1], wr / top, hinfo[2 * b], hinfo[2 * b + 1]);
+        fprintf(stderr, "[chfsi] iter %d job %d: theta0=%.6e theta_k=%.6e theta_p=%.6e maxres/theta0=%.3e info=%d,%d locked=%d\n",
+                iter, b, th[0], th[j.kmax - 1], th[j.p - 1], wr / top, hinfo[2 * b], hinfo[2 * b + 1], j.c);
       }
       if (hinfo[2 * b] != 0 || hinfo[2 * b + 1] != 0) {
         // the last filter pass collapsed the block (contamination by the top directions grew
@@ -342,11 +364,15 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
       }
       bool conv = true;
       double worst = 0.0;
+      int lock = -1;   // first unconverged wanted pair: the leading ones are locked
       for (int t = 0; t < j.kmax; ++t) {
         if (!std::isfinite(th[t]) || !std::isfinite(rs[t])) throw Error(TTN_ERR_NUMERIC, "non-finite Ritz pair (non-finite input?)");
         if (th[t] <= 1e-13 * top) break;   // numerically-zero directions are never kept (reading A4)
         worst = std::max(worst, rs[t]);
-        if (rs[t] > kResTol * top) conv = false;
+        if (rs[t] > kResTol * top) {
+          conv = false;
+          if (lock < 0) lock = t;
+        }
       }
       if (!(top > 0.0)) conv = true;   // zero Gram: nothing to resolve
       if (conv) { j.done = true; continue; }
@@ -366,9 +392,11 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
       const double kAmp = iter == 0 ? kAmpFirst : kAmpLater;
       const double eps = std::max(worst / top, 1e-16);
       const double xk = th[std::min(j.kmax, j.p) - 1];
+      j.c = std::max(lock, 0);   // locked columns are projected out explicitly, so only the
+      const double tu = th[j.c];  // largest UNLOCKED Ritz value bounds the contamination growth
       auto amp = [&](double x, int mm) { return std::fabs(cheb_value(x, mm, lo, cut, top) / cheb_value(cut, mm, lo, cut, top)); };
       int m = 4;
-      while (m < 48 && amp(xk, m) < kAmp && eps * amp(top, m + 2) <= kCondMax) m += 2;
+      while (m < 48 && amp(xk, m) < kAmp && eps * amp(tu, m + 2) <= kCondMax) m += 2;
       std::vector<double> cf;   // m, lo, cut, top
       cf.push_back(m); cf.push_back(lo); cf.push_back(cut); cf.push_back(top);
       coefs.push_back(cf);
@@ -376,7 +404,7 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
       std::vector<double> dsc(j.p);
       for (int t = 0; t < j.p; ++t) {
         const double v = cheb_value(th[t], m, lo, cut, top);
-        dsc[t] = (std::fabs(v) > 1e-12) ? 1.0 / v : (v < 0 ? -1e12 : 1e12);   // cap the dynamic range
+        dsc[t] = t < j.c ? 1.0 : (std::fabs(v) > 1e-12) ? 1.0 / v : (v < 0 ? -1e12 : 1e12);   // cap the dynamic range
       }
       TTN_CUDA(cudaMemcpyAsync(j.dscale, ctx->stager->put(dsc.data(), sizeof(double) * j.p), sizeof(double) * j.p,
                                cudaMemcpyDeviceToDevice, s));
@@ -390,6 +418,7 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
     int mmax = 0;
     for (auto& cf : coefs) mmax = std::max(mmax, (int)cf[0]);
     std::vector<double> sigma(act.size()), s1(act.size());
+    std::vector<cplx*> xb(act.size()), yb(act.size());   // recurrence buffers (tails of V and Y)
     {
       std::vector<GemmProblem> g;
       for (size_t q = 0; q < act.size(); ++q) {
@@ -398,9 +427,11 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
         const double e = 0.5 * (cut - lo), c = 0.5 * (cut + lo);
         s1[q] = e / (top - c);
         sigma[q] = s1[q];
-        GemmProblem gp = mk_gemm(j.Gs, OP_N, j.n, j.V, OP_N, j.p, j.Y, j.p, j.n, j.p, j.n);
+        GemmProblem gp = mk_gemm(j.Gs, OP_N, j.n, j.V + j.c, OP_N, j.p, j.Y + j.c, j.p, j.n, j.p - j.c, j.n);
         gp.alpha = make_double2(s1[q] / e, 0.0);
         g.push_back(gp);
+        xb[q] = j.V + j.c;
+        yb[q] = j.Y + j.c;
       }
       gemm_batch(ctx, g, st);
     }
@@ -412,18 +443,23 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
         const double lo = coefs[q][1], cut = coefs[q][2];
         const double e = 0.5 * (cut - lo);
         const double sn = 1.0 / (2.0 / s1[q] - sigma[q]);
-        // X <- (2 sn / e) Gs Y - sigma sn X   (X = V buffer), then swap roles
-        GemmProblem gp = mk_gemm(j.Gs, OP_N, j.n, j.Y, OP_N, j.p, j.V, j.p, j.n, j.p, j.n);
+        // X <- (2 sn / e) Gs Y - sigma sn X, then swap roles
+        GemmProblem gp = mk_gemm(j.Gs, OP_N, j.n, yb[q], OP_N, j.p, xb[q], j.p, j.n, j.p - j.c, j.n);
         gp.alpha = make_double2(2.0 * sn / e, 0.0);
         gp.beta = make_double2(-sigma[q] * sn, 0.0);
         g.push_back(gp);
         sigma[q] = sn;
-        std::swap(j.V, j.Y);
+        std::swap(xb[q], yb[q]);
       }
       gemm_batch(ctx, g, st);
     }
-    // filtered block is in Y
-    for (Job* jp : act) std::swap(jp->V, jp->Y);
+    // the newest filtered tail is yb; the locked columns live in V[:, 0:c]: bring it there
+    for (size_t q = 0; q < act.size(); ++q) {
+      Job& j = *act[q];
+      if (yb[q] != j.V + j.c)
+        TTN_CUDA(cudaMemcpy2DAsync(j.V + j.c, sizeof(cplx) * j.p, yb[q], sizeof(cplx) * j.p,
+                                   sizeof(cplx) * (size_t)(j.p - j.c), (size_t)j.n, cudaMemcpyDeviceToDevice, s));
+    }
     orth(act);
     rayleigh_ritz(act);
   }
