@@ -74,6 +74,30 @@ def make_instances(cfg, seeds):
     return [W.make_config(cfg, seed=s) for s in seeds]
 
 
+# ----------------------------------------------------------------------------- multi-rank
+def shard_seeds(rank, batch, partitioned):
+    """Instances of one rank: independent seeds rank*batch + 0..batch-1 (weak scaling), or the
+    same replicated instance(s) on every rank for a subtree-partitioned apply."""
+    return list(range(batch)) if partitioned else [rank * batch + i for i in range(batch)]
+
+
+def aggregate(ms, flops, applies, world, partitioned, device):
+    """Job totals over ranks: time = max over ranks; work = sum over ranks (independent
+    instances) or rank 0's (a partitioned apply does the same applies on every rank)."""
+    if world == 1:
+        return ms, flops, float(applies)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms, flops, float(applies)], dtype=torch.float64, device=device)
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = t.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    if partitioned:
+        return mx[0].item(), flops, float(applies)
+    return mx[0].item(), sm[1].item(), sm[2].item()
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     def __init__(self, path):
@@ -198,7 +222,7 @@ def run_native(args, rank, world, local_rank):
     # config 4 on N > 1 GPUs: ONE instance, partitioned over the ranks by subtrees (every rank
     # holds the same replicated inputs, ttn_ctx_set_comm); other configs: independent instances
     partitioned = cfg == 4 and world > 1
-    seeds = [i for i in range(batch)] if partitioned else [rank * batch + i for i in range(batch)]
+    seeds = shard_seeds(rank, batch, partitioned)
     insts = make_instances(cfg, seeds)
     stream = torch.cuda.Stream(local_rank)
     torch.cuda.set_stream(stream)
@@ -295,17 +319,7 @@ def run_native(args, rank, world, local_rank):
     P.ttn_profile_enable(False)
     clk = clocks.stop(local_rank) if clocks else None
 
-    t = torch.tensor([ms_total, flops, float(applies)], dtype=torch.float64, device=f"cuda:{local_rank}")
-    if world > 1:
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, flops_all, applies_all = mx[0].item(), sm[1].item(), sm[2].item()
-        if partitioned:   # the same applies on every rank: count them once
-            flops_all, applies_all = flops, float(applies)
-    else:
-        ms_max, flops_all, applies_all = ms_total, flops, float(applies)
+    ms_max, flops_all, applies_all = aggregate(ms_total, flops, applies, world, partitioned, f"cuda:{local_rank}")
 
     # ------------------------------------------------------------------ e2e (host buffers)
     e2e = None

@@ -270,3 +270,54 @@ def test_config4_t3ns_matches_oracle_golden(P, ctx):
         d_cos, d_rel = distances(phi_g, phi_o)
         print(f"config 4 full parity: 1-cos={d_cos:.3e} rel={d_rel:.3e}")
         assert d_cos <= 1e-10, (d_cos, d_rel)
+
+
+def test_config3_full_batch_as_benched(P, ctx):
+    """Config 3 in bench.py's launch configuration (one cbc_apply_batch over seeds 0..63):
+    oracle parity on sampled instances, isometry (P3) and the report's norm on all 64."""
+    seeds = list(range(64))
+    insts = [W.make_config(3, seed=s) for s in seeds]
+    pairs = [gpu_pair(P, ctx, i) for i in insts]
+    outs, reps = P.cbc_apply_batch(ctx, [p[0] for p in pairs], [p[1] for p in pairs], 32)
+    for s, (inst, out, rep) in enumerate(zip(insts, outs, reps)):
+        phi_g = to_oracle(P, out, inst.parent)
+        if s in (0, 21, 42, 63):
+            op_o, psi_o = oracle_pair(inst)
+            _check(phi_g, oracle_cbc(op_o, psi_o, 32), op_o, psi_o, rep)
+            continue
+        for i, t in enumerate(phi_g.tensors):
+            if i == phi_g.root:
+                continue
+            q = np.moveaxis(t, 1, -1).reshape(-1, t.shape[1])
+            assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
+        assert abs(rep["norm"] - np.linalg.norm(phi_g.tensors[phi_g.root])) <= 1e-12 * rep["norm"]
+
+
+def test_config5_full_batch_as_benched(P, ctx):
+    """Config 5 in bench.py's launch configuration (64 seeds x 10 layers, 4 worker streams):
+    the untruncated layers keep ||phi|| = 1 for every seed (P13); sampled seeds vs oracle."""
+    seeds = list(range(64))
+    parent = W.complete_binary(63)
+    insts = [W.make_config(5, seed=s) for s in seeds]
+    cur = [P.ttn_create(ctx, P.TTN_STATE, parent, i.phys, i.state_bond, i.state) for i in insts]
+    sample = {0: None, 63: None}
+    for s in sample:
+        sample[s] = TTN(parent, [t.copy() for t in insts[s].state])
+    P.ttn_ctx_set_workers(ctx, 4)
+    try:
+        for layer in range(10):
+            ops = []
+            for s in seeds:
+                o, ob, _ = W.circuit_layer_operator(parent, s, layer)
+                ops.append(P.ttn_create(ctx, P.TTN_OPERATOR, parent, [2] * 63, ob, o))
+                if s in sample:
+                    sample[s] = oracle_cbc(TTN(parent, o, "operator"), sample[s], 256)
+            cur, reps = P.cbc_apply_batch(ctx, ops, cur, 256)
+            for r in reps:
+                assert abs(r["norm"] - 1.0) <= 1e-12
+    finally:
+        P.ttn_ctx_set_workers(ctx, 1)
+    for s, po in sample.items():
+        g = to_oracle(P, cur[s], parent)
+        assert g.bonds() == po.bonds()
+        assert distances(g, po)[0] <= 1e-10

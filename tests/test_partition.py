@@ -149,3 +149,36 @@ def test_partitioned_config4_matches_golden():
         assert abs(norm(phi) ** 2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"]
     finally:
         ctx.close()
+
+
+def _bench_worker(rank, world, port, out):
+    import sys
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        seeds = bench.shard_seeds(rank, 64, False)
+        ms = 100.0 + 10.0 * rank          # rank 1 is the slower one
+        weak = bench.aggregate(ms, 1e12, 64, world, False, "cpu")
+        strong = bench.aggregate(ms, 5e12, 1, world, True, "cpu")
+        out[rank] = (seeds, weak, strong, bench.shard_seeds(rank, 1, True))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_gloo_ranks_bench_sharding_and_max_over_ranks():
+    """bench.py's N > 1 logic on CPU: disjoint seed shards (weak scaling), max-over-ranks time,
+    summed work; a partitioned apply counts its replicated applies once."""
+    import torch.multiprocessing as mp
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_bench_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    (s0, w0, p0, r0), (s1, w1, p1, r1) = out[0], out[1]
+    assert sorted(s0 + s1) == list(range(128)) and not set(s0) & set(s1)
+    assert w0 == w1 == (110.0, 2e12, 128.0)
+    assert p0 == p1 == (110.0, 5e12, 1.0)
+    assert r0 == r1 == [0]
