@@ -133,6 +133,13 @@ TTN_API ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const
 /* <a|b>, conjugate-linear in a, by a leaves-to-root environment sweep; a and b share the
  * parent array and physical dimensions, bonds may differ.  Synchronises the stream.      */
 TTN_API ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out);
+/* <bra| op |ket> (one leaves-to-root sweep through bra*, op, ket); all three on one parent
+ * array and physical dimensions.  With bra = cbc_apply(op, ket) this is the projection
+ * identity <phi|O|psi> = ||phi||^2 (phi = W W^dagger O psi).  Synchronises the stream.     */
+TTN_API ttn_status ttn_sandwich(ttn_ctx ctx, ttn bra, ttn op, ttn ket, ttn_c128* out);
+/* ||op |ket>||^2 = <ket| op^dagger op |ket> by one sweep (environments carry four legs), so
+ * the truncation error eps^2 = 1 - ||phi||^2 / ||O psi||^2 (A19) needs no dense vector.     */
+TTN_API ttn_status ttn_op_norm2(ttn_ctx ctx, ttn op, ttn ket, double* out);
 /* Batched overlaps <a_j|b_j>, j < n.                                                      */
 TTN_API ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b, ttn_c128* out);
 /* Split every later cbc_apply_batch of >= 2n instances on ctx into n concurrent sub-batches,

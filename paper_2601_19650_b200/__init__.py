@@ -177,6 +177,20 @@ def ttn_overlap_batch(ctx: Context, a: Sequence[TTN], b: Sequence[TTN]) -> List[
     return [complex(out[i].re, out[i].im) for i in range(n)]
 
 
+def ttn_sandwich(ctx: Context, bra: TTN, op: TTN, ket: TTN) -> complex:
+    """<bra| op |ket> (include/ttn_cbc.h)."""
+    v = L.c128()
+    L.check(ctx.h, L.load().ttn_sandwich(ctx.h, bra.h, op.h, ket.h, C.byref(v)))
+    return complex(v.re, v.im)
+
+
+def ttn_op_norm2(ctx: Context, op: TTN, ket: TTN) -> float:
+    """||op |ket>||^2 = <ket| op^dagger op |ket>."""
+    v = C.c_double()
+    L.check(ctx.h, L.load().ttn_op_norm2(ctx.h, op.h, ket.h, C.byref(v)))
+    return v.value
+
+
 def ttn_profile_enable(on: bool = True) -> None:
     L.check(None, L.load().ttn_profile_enable(int(bool(on))))
 

@@ -21,7 +21,8 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_TOPOLOGY", 3: "ERR_SHAPE", 4: "ERR_OOM"
 SYMBOLS = ["ttn_ctx_create", "ttn_ctx_destroy", "ttn_last_error", "ttn_version", "ttn_create", "ttn_destroy",
            "ttn_n_nodes", "ttn_node_shape", "ttn_get_tensor", "cbc_apply", "cbc_apply_batch", "ttn_overlap",
            "ttn_overlap_batch", "ttn_norm", "ttn_get_data", "ttn_profile_enable", "ttn_profile_read", "ttn_launch_count",
-           "ttn_comm_unique_id", "ttn_ctx_set_comm", "ttn_partition_plan", "ttn_ctx_set_workers"]
+           "ttn_comm_unique_id", "ttn_ctx_set_comm", "ttn_partition_plan", "ttn_ctx_set_workers",
+           "ttn_sandwich", "ttn_op_norm2"]
 
 
 class c128(C.Structure):
@@ -77,6 +78,8 @@ def load():
         "ttn_launch_count": (C.c_int, [C.POINTER(I64)]),
         "ttn_comm_unique_id": (C.c_int, [P]),
         "ttn_ctx_set_workers": (C.c_int, [P, C.c_int]),
+        "ttn_sandwich": (C.c_int, [P, P, P, P, C.POINTER(c128)]),
+        "ttn_op_norm2": (C.c_int, [P, P, P, C.POINTER(D)]),
         "ttn_ctx_set_comm": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int]),
         "ttn_partition_plan": (C.c_int, [I32, C.POINTER(I32), C.c_int, C.POINTER(I32)]),
     }

@@ -279,6 +279,40 @@ ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const ttn* b,
 
 ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out) { return ttn_overlap_batch(ctx, 1, &a, &b, out); }
 
+ttn_status ttn_sandwich(ttn_ctx ctx, ttn bra, ttn op, ttn ket, ttn_c128* out) {
+  if (!ctx || !bra || !op || !ket || !out) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    const ttn_s* b[1] = {bra};
+    const ttn_s* o[1] = {op};
+    const ttn_s* k[1] = {ket};
+    std::vector<SweepLayer> L(3);
+    L[0].h = b; L[0].conj = true;
+    L[1].h = o; L[1].op = true;
+    L[2].h = k;
+    cplx r;
+    sweep_impl(ctx, 1, L, &r);
+    *out = ttn_c128{r.x, r.y};
+  });
+}
+
+ttn_status ttn_op_norm2(ttn_ctx ctx, ttn op, ttn ket, double* out) {
+  if (!ctx || !op || !ket || !out) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    const ttn_s* o[1] = {op};
+    const ttn_s* k[1] = {ket};
+    std::vector<SweepLayer> L(4);
+    L[0].h = k; L[0].conj = true;
+    L[1].h = o; L[1].op = true; L[1].conj = true; L[1].dagger = true;
+    L[2].h = o; L[2].op = true;
+    L[3].h = k;
+    cplx r;
+    sweep_impl(ctx, 1, L, &r);
+    *out = r.x;
+  });
+}
+
 ttn_status ttn_ctx_set_workers(ttn_ctx ctx, int n) {
   if (!ctx || n < 1 || n > 64) return TTN_ERR_ARG;
   DeviceGuard g(ctx->device);

@@ -726,4 +726,97 @@ void overlap_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* a, const ttn_s* co
   ctx->env.reset();
 }
 
+// <bra| O_1 ... O_m |ket> by one leaves-to-root environment sweep: every node contracts its
+// layer tensors (conj(bra), the operators, ket) with the children's environments (one leg
+// per layer) into its parent-edge environment, through the same batched contraction engine.
+// An operator layer with `dagger` enters as conj(O) with its physical legs swapped (O^dagger).
+// Used for <phi|O|psi> (the projection identity P2 at full size) and ||O psi||^2 =
+// <psi|O^dagger O|psi> (the truncation error eps^2 = 1 - ||phi||^2 / ||O psi||^2, A19).
+void sweep_impl(ttn_ctx_s* ctx, int nb, const std::vector<SweepLayer>& layers, cplx* out) {
+  const int nl = (int)layers.size();
+  if (nl < 2 || layers.front().op || layers.back().op) throw Error(TTN_ERR_ARG, "sweep: bra and ket must be states");
+  const ttn_s* ref = layers[0].h[0];
+  for (int j = 0; j < nb; ++j)
+    for (const auto& Ly : layers) {
+      const ttn_s* t = Ly.h[j];
+      if (!t) throw Error(TTN_ERR_ARG, "NULL handle");
+      if ((t->kind == TTN_OPERATOR) != Ly.op) throw Error(TTN_ERR_ARG, "sweep: operator / state handle expected");
+      if (t->parent != ref->parent) throw Error(TTN_ERR_TOPOLOGY, "topology mismatch");
+      if (t->phys != ref->phys) throw Error(TTN_ERR_SHAPE, "leg mismatch: physical dimensions");
+    }
+  const int n = ref->n;
+  int maxd = 0;
+  for (int i = 0; i < n; ++i) maxd = std::max(maxd, ref->depth[i]);
+  ctx->scratch.reset();
+  ctx->env.reset();
+  // environment of node i: one leg per layer (that layer's parent-edge bond)
+  std::vector<cplx*> E((size_t)nb * n, nullptr);
+  std::vector<std::vector<int64_t>> Edims((size_t)nb * n);
+  ExecStats st;
+  auto PHY = [](int k) { return 1 + k; };              // physical label between layers k-1 and k
+  auto VIR = [](int k, int leg) { return 100 * (k + 1) + leg; };
+  for (int L = maxd; L >= 0; --L) {
+    std::vector<Task> tasks;
+    for (int j = 0; j < nb; ++j)
+      for (int i = 0; i < n; ++i) {
+        if (ref->depth[i] != L) continue;
+        Task t;
+        int pk = 0;   // physical label index above the current layer
+        for (int k = 0; k < nl; ++k) {
+          const SweepLayer& Ly = layers[k];
+          const ttn_s* h = Ly.h[j];
+          Operand X;
+          X.ptr = h->node(i);
+          X.dims = h->shape[i];
+          X.conj = Ly.conj;
+          size_t v0;
+          if (!Ly.op) {
+            X.labels.push_back(PHY(pk));
+            v0 = 1;
+          } else {
+            // O[out, in, ...]: plain O maps the label below (pk+1) to the one above (pk);
+            // O^dagger = conj(O) with out / in swapped
+            X.labels.push_back(Ly.dagger ? PHY(pk + 1) : PHY(pk));
+            X.labels.push_back(Ly.dagger ? PHY(pk) : PHY(pk + 1));
+            ++pk;
+            v0 = 2;
+          }
+          for (size_t l = v0; l < X.dims.size(); ++l) X.labels.push_back(VIR(k, (int)(l - v0)));
+          t.ops.push_back(X);
+        }
+        for (size_t c = 0; c < ref->children[i].size(); ++c) {
+          const size_t ci = (size_t)j * n + ref->children[i][c];
+          Operand F;
+          F.ptr = E[ci];
+          F.dims = Edims[ci];
+          for (int k = 0; k < nl; ++k) F.labels.push_back(VIR(k, 1 + (int)c));
+          t.ops.push_back(F);
+        }
+        std::vector<int64_t> od;
+        int64_t tot = 1;
+        for (int k = 0; k < nl; ++k) {
+          t.out_labels.push_back(VIR(k, 0));
+          const int64_t e = layers[k].h[j]->shape[i][layers[k].op ? 2 : 1];
+          od.push_back(e);
+          tot *= e;
+        }
+        const size_t me = (size_t)j * n + i;
+        E[me] = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * std::max<int64_t>(tot, 1)));
+        Edims[me] = od;
+        t.out = E[me];
+        tasks.push_back(t);
+      }
+    contract_batch(ctx, tasks, st);
+    ctx->scratch.reset();
+  }
+  ctx->ensure_small(sizeof(cplx) * nb);
+  cplx* h = reinterpret_cast<cplx*>(ctx->hbuf);
+  for (int j = 0; j < nb; ++j)
+    TTN_CUDA(cudaMemcpyAsync(h + j, E[(size_t)j * n + ref->root], sizeof(cplx), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  TTN_CUDA(cudaGetLastError());
+  for (int j = 0; j < nb; ++j) out[j] = h[j];
+  ctx->env.reset();
+}
+
 }  // namespace tcbc

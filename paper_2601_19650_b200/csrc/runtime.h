@@ -109,6 +109,12 @@ void free_ttn(ttn_s* t);
 void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts,
                     int64_t max_bond, double tol, ttn_s** outs, ttn_cbc_report* reps);
 void overlap_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* a, const ttn_s* const* b, cplx* out);
+// One layer of a <bra| O_1 ... O_m |ket> sweep (per-instance handles).
+struct SweepLayer {
+  const ttn_s* const* h;
+  bool op = false, conj = false, dagger = false;
+};
+void sweep_impl(ttn_ctx_s* ctx, int nb, const std::vector<SweepLayer>& layers, cplx* out);
 // Subtree groups of a parts-way partitioned apply (group -1: replicated top); cuts_out gets
 // the subtree roots.  Host-only.
 std::vector<int> partition_groups(const ttn_s* ref, int parts, std::vector<int>* cuts_out);

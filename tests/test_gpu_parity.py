@@ -321,3 +321,43 @@ def test_config5_full_batch_as_benched(P, ctx):
         g = to_oracle(P, cur[s], parent)
         assert g.bonds() == po.bonds()
         assert distances(g, po)[0] <= 1e-10
+
+
+def test_sandwich_and_op_norm2_match_oracle(P, ctx):
+    from oracle import sandwich
+    for parent, chi, D in ((W.complete_binary(7), 3, 2), (W.chain(6), 4, 3), (W.t_tree(2), 3, 2)):
+        n = len(parent)
+        a = W.configs.random_instance(parent, [2] * n, chi, D, 4, seed=31)
+        b = W.configs.random_instance(parent, [2] * n, chi + 1, D, 4, seed=32)
+        ha = P.ttn_create(ctx, P.TTN_STATE, parent, a.phys, a.state_bond, a.state)
+        hb = P.ttn_create(ctx, P.TTN_STATE, parent, b.phys, b.state_bond, b.state)
+        ho = P.ttn_create(ctx, P.TTN_OPERATOR, parent, a.phys, a.op_bond, a.op)
+        A, B, O = TTN(parent, a.state), TTN(parent, b.state), TTN(parent, a.op, "operator")
+        ref = sandwich(A, O, B)
+        got = P.ttn_sandwich(ctx, ha, ho, hb)
+        assert abs(got - ref) <= 1e-12 * abs(ref), (got, ref)
+        on2 = norm(exact_apply(O, B)) ** 2
+        assert abs(P.ttn_op_norm2(ctx, ho, hb) - on2) <= 1e-12 * on2
+
+
+def test_projection_identity_and_eps2_on_gpu_full_size(P, ctx):
+    """P2 <phi|O|psi> = ||phi||^2 and eps^2 = 1 - ||phi||^2/||O psi||^2 computed entirely on the
+    GPU (ttn_sandwich, ttn_op_norm2) at config-3 and config-4 sizes; eps^2 against the oracle
+    (config 3) and the truncation bound 0 <= eps^2 < 1."""
+    import json
+    import os
+    for k, seed in ((3, 5), (4, 0)):
+        inst = W.make_config(k, seed=seed)
+        op_g, st_g = gpu_pair(P, ctx, inst)
+        out, rep = P.cbc_apply(ctx, op_g, st_g, inst.max_bond)
+        n2 = rep["norm"] ** 2
+        s = P.ttn_sandwich(ctx, out, op_g, st_g)
+        assert abs(s - n2) <= 1e-11 * n2, (k, s, n2)
+        on2 = P.ttn_op_norm2(ctx, op_g, st_g)
+        e2 = 1.0 - n2 / on2
+        assert 0.0 <= e2 < 1.0
+        if k == 3:
+            op_o, psi_o = oracle_pair(inst)
+            phi_o = oracle_cbc(op_o, psi_o, inst.max_bond)
+            e2_o = 1.0 - norm(phi_o) ** 2 / norm(exact_apply(op_o, psi_o)) ** 2
+            assert abs(e2 - e2_o) <= 1e-10, (e2, e2_o)
