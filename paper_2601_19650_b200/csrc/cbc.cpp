@@ -97,6 +97,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   std::vector<ScaleRowsProblem> sr;
   int* d_k = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nj));
   double* d_w = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nj));
+  int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nj));   // pow2 range exponents
+  std::vector<Pow2Problem> p2(nj);
   std::vector<int64_t> kmaxs(nj);
   for (int j = 0; j < nj; ++j) {
     CompressJob& J = jobs[j];
@@ -122,6 +124,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     h.tau = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn));
     h.tol2 = tol * tol;
     h.floor_rel = kRankFloor;
+    h.exp2 = d_e + j;
+    p2[j] = Pow2Problem{const_cast<cplx*>(J.X), m * n, d_e + j};
     h.max_bond = (int)std::min<int64_t>(max_bond, INT32_MAX);
     flops_inst[J.inst] += 8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * kmax);
     // factor storage (kmax rows; the first k are the factor)
@@ -138,7 +142,9 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     }
     st.peak_entries = std::max(st.peak_entries, nn * nn);
   }
+  launch_pow2_normalize(p2.data(), nj, *ctx->stager, ctx->stream);   // the Gram squares X
   gemm_batch(ctx, grams, st);
+  launch_pow2_restore(p2.data(), nj, *ctx->stager, ctx->stream);     // the K-route factor reads X
   static const bool dump = getenv("TTN_DEBUG_HEEV") && std::string(getenv("TTN_DEBUG_HEEV")) == "3";
   std::vector<std::vector<cplx>> gcopy;
   if (dump) {   // debug: keep the Grams (heev destroys them) to dump the ones that fail
@@ -248,6 +254,15 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
   }
   if (!eyes.empty()) launch_eye(eyes.data(), (int)eyes.size(), *ctx->stager, ctx->stream);
   if (tall.empty()) return 0;
+  {   // W = S^H S squares S: bring S into range first (Q is invariant under S -> c S, c > 0)
+    int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * tall.size()));
+    std::vector<Pow2Problem> p2;
+    for (size_t q = 0; q < tall.size(); ++q) {
+      QRJob& J = jobs[tall[q]];
+      p2.push_back(Pow2Problem{const_cast<cplx*>(J.S), J.m * J.kd, d_e + q});
+    }
+    launch_pow2_normalize(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
+  }
   gemm_batch(ctx, g1, st);
   launch_potrf(p1.data(), (int)p1.size(), *ctx->stager, ctx->stream);
   launch_trtri(t1.data(), (int)t1.size(), *ctx->stager, ctx->stream);

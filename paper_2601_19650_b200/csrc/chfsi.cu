@@ -146,9 +146,10 @@ __global__ void large_finish(FinDev* P, int nprob) {
       k = cnt < 1 ? 1 : (cnt > H.max_bond ? H.max_bond : cnt);
       for (int t = 0; t < k; ++t) kept += F.theta[t];
     }
-    for (int t = 0; t < kmax; ++t) H.lam[t] = (t < k && trace > 0.0 && l1 > 0.0) ? F.theta[t] : 0.0;
+    const int e2 = H.exp2 ? 2 * pow2_effective(*H.exp2) : 0;   // back to the unscaled Gram
+    for (int t = 0; t < kmax; ++t) H.lam[t] = (t < k && trace > 0.0 && l1 > 0.0) ? ldexp(F.theta[t], e2) : 0.0;
     if (H.k_out) *H.k_out = k;
-    if (H.w_out) *H.w_out = fmax(trace - kept, 0.0);
+    if (H.w_out) *H.w_out = ldexp(fmax(trace - kept, 0.0), e2);
   }
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)kmax * n;
        i += (long long)gridDim.x * blockDim.x) {

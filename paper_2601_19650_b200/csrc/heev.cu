@@ -974,6 +974,18 @@ __global__ void heev_backtr(const HeevProblem* __restrict__ probs, int nprob, in
   }
 }
 
+// K7: eigenvalues and discarded weight back to the unscaled data (HeevProblem::exp2)
+__global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nprob) return;
+  const HeevProblem& P = probs[i];
+  if (!P.exp2) return;
+  const int e = pow2_effective(*P.exp2);
+  if (e == 0) return;
+  for (int t = 0; t < P.kmax; ++t) P.lam[t] = ldexp(P.lam[t], 2 * e);
+  if (P.w_out) *P.w_out = ldexp(*P.w_out, 2 * e);
+}
+
 // ---------------------------------------------------------------- K6: truncation decision
 __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1266,6 +1278,8 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
     }
   }
   heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+  heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n);
+  count_launch();
   count_launch(); count_launch(); count_launch(); count_launch(); count_launch();
   prof_end(s, "heev", fl, by);
 }

@@ -77,6 +77,8 @@ struct HeevProblem {
   double floor_rel;    // rank floor on lam / lam_1
   int max_bond;
   int estart;          // filled by the launcher: prefix sum of kmax (eigenpair task index)
+  const int* exp2;     // may be null: A was formed from data scaled by 2^-e (pow2_normalize);
+                       // the returned eigenvalues and discarded weight are scaled by 2^(2e)
 };
 size_t heev_work_doubles(int n, int kmax);
 size_t heev_smem_bytes(int n, int kmax);
@@ -138,6 +140,16 @@ void launch_geqr_q(GeqrProblem* h, int n, Stager& st, cudaStream_t s);
 // P[i*ld + j] = (i == j) for i < m, j < ncols, grouped
 struct EyeProblem { cplx* p; int m; int ncols; long long start; };
 void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s);
+
+// Exact power-of-two range control (PAPER.md's CBC is scale covariant, pin P12): Grams and
+// CholeskyQR square their inputs, so data whose largest entry is beyond 2^+-200 (positive-bias
+// random networks reach 1e80) is scaled by 2^-e before the square and back after.
+// e is the largest binary exponent of the problem's entries, kept in *exp (device);
+// pow2_effective(e) = 0 when no scaling is needed (then the data is untouched).
+struct Pow2Problem { cplx* x; long long len; int* exp; };
+void launch_pow2_normalize(Pow2Problem* h, int n, Stager& st, cudaStream_t s);   // x *= 2^-e
+void launch_pow2_restore(Pow2Problem* h, int n, Stager& st, cudaStream_t s);     // x *= 2^+e
+__host__ __device__ inline int pow2_effective(int e) { return (e < -2000 || (e > -100 && e < 100)) ? 0 : e; }
 
 // Counters of kernel launches issued by this library (for the bench's gpu_launches claim).
 long long launch_count();

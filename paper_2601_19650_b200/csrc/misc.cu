@@ -97,6 +97,31 @@ int grid_for(long long total, int threads) {
   return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 16));
 }
 
+__global__ void pow2_maxexp(const Pow2Problem* __restrict__ probs) {
+  const Pow2Problem& P = probs[blockIdx.y];
+  int e = -2147483000;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.len; i += (long long)gridDim.x * blockDim.x) {
+    const cplx v = P.x[i];
+    const double m = fmax(fabs(v.x), fabs(v.y));
+    if (m > 0.0) e = max(e, ilogb(m));
+  }
+  for (int o = 16; o > 0; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+  if ((threadIdx.x & 31) == 0 && e > -2147483000) atomicMax(P.exp, e);
+}
+
+__global__ void pow2_scale(const Pow2Problem* __restrict__ probs, int sign) {
+  const Pow2Problem& P = probs[blockIdx.y];
+  const int e = pow2_effective(*P.exp);
+  if (e == 0) return;
+  const int sh = sign * e;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.len; i += (long long)gridDim.x * blockDim.x) {
+    cplx v = P.x[i];
+    v.x = ldexp(v.x, sh);
+    v.y = ldexp(v.y, sh);
+    P.x[i] = v;
+  }
+}
+
 }  // namespace
 
 void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s) {
@@ -152,6 +177,36 @@ void launch_fill(cplx* p, long long n, cplx v, cudaStream_t s) {
   prof_begin(s);
   fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
   prof_end(s, "misc", 0.0, 16.0 * (double)n);
+  count_launch();
+}
+
+void launch_pow2_normalize(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  long long mx = 1;
+  bool contiguous = true;
+  for (int i = 0; i < n; ++i) {
+    mx = std::max(mx, h[i].len);
+    contiguous = contiguous && h[i].exp == h[0].exp + i;
+  }
+  // 0x80808080: below every binary exponent (one memset when the exponents are contiguous)
+  if (contiguous) cudaMemsetAsync(h[0].exp, 0x80, sizeof(int) * n, s);
+  else
+    for (int i = 0; i < n; ++i) cudaMemsetAsync(h[i].exp, 0x80, sizeof(int), s);
+  const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
+  const unsigned gx = (unsigned)std::min<long long>((mx + 255) / 256, 296);
+  pow2_maxexp<<<dim3(gx, n), 256, 0, s>>>(d);
+  pow2_scale<<<dim3(gx, n), 256, 0, s>>>(d, -1);
+  count_launch();
+  count_launch();
+}
+
+void launch_pow2_restore(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  long long mx = 1;
+  for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].len);
+  const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
+  const unsigned gx = (unsigned)std::min<long long>((mx + 255) / 256, 296);
+  pow2_scale<<<dim3(gx, n), 256, 0, s>>>(d, +1);
   count_launch();
 }
 

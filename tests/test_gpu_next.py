@@ -115,3 +115,22 @@ def test_f4_positive_bias_entries(P, ctx, mb):
     assert phi_g.bonds() == phi_o.bonds()
     assert distances(phi_g, phi_o)[0] <= 1e-10
     assert abs(norm(phi_g) - norm(phi_o)) <= 1e-10 * norm(phi_o)
+
+
+@pytest.mark.parametrize("kind,mb", [("mps", 6), ("ttree", 4), ("binary", 4), ("ftps", 4)])
+def test_f2_paper_random_structures_vs_oracle(P, ctx, kind, mb):
+    """f2: the paper's random benchmark structures (U[-0.5, 1] entries, d = 3) at a
+    small target bond, GPU vs oracle; eps^2 from ttn_op_norm2 vs the oracle's dense-free sweep."""
+    import workloads.paper as WP
+    from oracle import sandwich
+    inst = WP.paper_random_instance(kind, mb, seed=1)
+    op_g, st_g = gpu_pair(P, ctx, inst)
+    out, rep = P.cbc_apply(ctx, op_g, st_g, mb)
+    phi_g = to_oracle(P, out, inst.parent)
+    op_o, psi_o = oracle_pair(inst)
+    phi_o = oracle_cbc(op_o, psi_o, mb)
+    assert phi_g.bonds() == phi_o.bonds()
+    assert distances(phi_g, phi_o)[0] <= 1e-10
+    assert abs(norm(phi_g) ** 2 - norm(phi_o) ** 2) <= 1e-10 * norm(phi_o) ** 2
+    s = P.ttn_sandwich(ctx, out, op_g, st_g)                 # P2 on the GPU
+    assert abs(s - rep["norm"] ** 2) <= 1e-11 * rep["norm"] ** 2
