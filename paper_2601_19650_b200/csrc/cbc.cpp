@@ -41,6 +41,7 @@ struct CompressJob {
   Fac* dst;
   int64_t a, b;      // column legs of X (n = a*b)
   int inst;
+  int* exp = nullptr;   // max binary exponent of X, written by the producing GEMM (or null)
 };
 
 struct QRJob {
@@ -48,6 +49,7 @@ struct QRJob {
   int64_t m, kd;
   cplx* Q;           // m x r output, r = min(m, kd)
   int inst;
+  int* exp = nullptr;   // max binary exponent of S, written by the producing GEMM
 };
 
 Task node_task(const ttn_s* st, const ttn_s* op, int i, const std::map<int, const Fac*>& facs, int open_leg,
@@ -124,8 +126,9 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     h.tau = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn));
     h.tol2 = tol * tol;
     h.floor_rel = kRankFloor;
-    h.exp2 = d_e + j;
-    p2[j] = Pow2Problem{const_cast<cplx*>(J.X), m * n, d_e + j};
+    int* ej = J.exp ? J.exp : d_e + j;
+    h.exp2 = ej;
+    p2[j] = Pow2Problem{const_cast<cplx*>(J.X), m * n, ej};
     h.max_bond = (int)std::min<int64_t>(max_bond, INT32_MAX);
     flops_inst[J.inst] += 8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * kmax);
     // factor storage (kmax rows; the first k are the factor)
@@ -142,7 +145,12 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     }
     st.peak_entries = std::max(st.peak_entries, nn * nn);
   }
-  launch_pow2_normalize(p2.data(), nj, *ctx->stager, ctx->stream);   // the Gram squares X
+  {   // the Gram squares X: exponents from the producing GEMM's epilogue where available
+    std::vector<Pow2Problem> have, need;
+    for (int j = 0; j < nj; ++j) (jobs[j].exp ? have : need).push_back(p2[j]);
+    launch_pow2_apply(have.data(), (int)have.size(), *ctx->stager, ctx->stream);
+    launch_pow2_normalize(need.data(), (int)need.size(), *ctx->stager, ctx->stream);
+  }
   gemm_batch(ctx, grams, st);
   launch_pow2_restore(p2.data(), nj, *ctx->stager, ctx->stream);     // the K-route factor reads X
   static const bool dump = getenv("TTN_DEBUG_HEEV") && std::string(getenv("TTN_DEBUG_HEEV")) == "3";
@@ -256,12 +264,14 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
   if (tall.empty()) return 0;
   {   // W = S^H S squares S: bring S into range first (Q is invariant under S -> c S, c > 0)
     int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * tall.size()));
-    std::vector<Pow2Problem> p2;
+    std::vector<Pow2Problem> have, need;
     for (size_t q = 0; q < tall.size(); ++q) {
       QRJob& J = jobs[tall[q]];
-      p2.push_back(Pow2Problem{const_cast<cplx*>(J.S), J.m * J.kd, d_e + q});
+      if (J.exp) have.push_back(Pow2Problem{const_cast<cplx*>(J.S), J.m * J.kd, J.exp});
+      else need.push_back(Pow2Problem{const_cast<cplx*>(J.S), J.m * J.kd, d_e + q});
     }
-    launch_pow2_normalize(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
+    launch_pow2_apply(have.data(), (int)have.size(), *ctx->stager, ctx->stream);
+    launch_pow2_normalize(need.data(), (int)need.size(), *ctx->stager, ctx->stream);
   }
   gemm_batch(ctx, g1, st);
   launch_potrf(p1.data(), (int)p1.size(), *ctx->stager, ctx->stream);
@@ -424,6 +434,12 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
           jobs.push_back(CompressJob{nullptr, 0, 0, &up[(size_t)b * n + i], sts[b]->shape[i][1], ops[b]->shape[i][2], b});
         }
       if (tasks.empty()) continue;
+      int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * tasks.size()));
+      pow2_reset(d_e, (int)tasks.size(), ctx->stream);
+      for (size_t j = 0; j < tasks.size(); ++j) {
+        tasks[j].out_exp = d_e + j;
+        jobs[j].exp = d_e + j;
+      }
       ExecStats cs;
       contract_batch(ctx, tasks, cs);
       for (size_t j = 0; j < tasks.size(); ++j) {
@@ -459,6 +475,12 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
           }
         }
       if (tasks.empty()) continue;
+      int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * tasks.size()));
+      pow2_reset(d_e, (int)tasks.size(), ctx->stream);
+      for (size_t j = 0; j < tasks.size(); ++j) {
+        tasks[j].out_exp = d_e + j;
+        jobs[j].exp = d_e + j;
+      }
       ExecStats cs;
       contract_batch(ctx, tasks, cs);
       for (size_t j = 0; j < tasks.size(); ++j) {
@@ -575,6 +597,8 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       std::vector<GemmProblem> sg, rg;
       std::vector<QRJob> qj;
       std::vector<PermProblem> pq;
+      int* s_exp = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * tasks.size()));   // max exponents of S
+      pow2_reset(s_exp, (int)tasks.size(), ctx->stream);
       for (size_t j = 0; j < tasks.size(); ++j) {
         const int b = who[j].first, i = who[j].second;
         if (i == root) continue;
@@ -584,10 +608,12 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
         for (auto d : tasks[j].out_dims) tot *= d;
         const int64_t ms = tot / nz, kd = fd.k, r = rb[b][i];
         cplx* S = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * kd));
+        int* se = s_exp + j;
         sg.push_back(mk_gemm(tasks[j].out, OP_N, nz, fd.p, OP_T, nz, S, kd, ms, kd, nz));   // S = Z Fd^T (Eq. 12 via Z)
+        sg.back().exp_out = se;
         acc_f(sub)[b] += 8.0 * (double)ms * kd * nz;
         cplx* Q = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * ms * r));
-        qj.push_back(QRJob{S, ms, kd, Q, b});
+        qj.push_back(QRJob{S, ms, kd, Q, b, se});
         // T'_i = Q in ABI order [d, r, r_c...]: Q viewed as [d, Rc, r] -> [d, r, Rc]
         const int64_t d = ref->phys[i], Rc = ms / d;
         PermProblem pp{};

@@ -379,6 +379,7 @@ void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st) {
       cplx* C = s.to_out ? tasks[i].out
                          : static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * std::max<int64_t>(s.res_elems, 1)));
       g.C = C;
+      if (s.to_out) g.exp_out = tasks[i].out_exp;
       slot[i][P.nin + r] = C;
       round.push_back(g);
     }

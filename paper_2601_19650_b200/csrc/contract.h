@@ -24,6 +24,7 @@ struct Task {
   std::vector<Operand> ops;
   std::vector<int> out_labels;
   cplx* out = nullptr;                 // destination; allocated from ctx->scratch when null
+  int* out_exp = nullptr;              // optional: max binary exponent of the output (GEMM epilogue)
   std::vector<int64_t> out_dims;       // filled by contract_batch
   double flops = 0.0;                  // filled by contract_batch (8 * complex MACs)
 };

@@ -67,6 +67,12 @@ __device__ __forceinline__ double neg_if(double x, bool neg) {
   return neg ? __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x)) : x;
 }
 
+// binary exponent of a double from its bit pattern (zero / denormal: "no data")
+__device__ __forceinline__ int bexp(double x) {
+  const int be = (__double2hiint(x) >> 20) & 0x7ff;
+  return be ? be - 1023 : -2147483000;
+}
+
 // offset of multi-index x in a group of n legs (row-major: last leg fastest); the outermost
 // leg needs no division
 __device__ __forceinline__ long long goff(int x, int n, const int* d, const long long* s) {
@@ -290,6 +296,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
   const cplx al = P.alpha, be = P.beta;
   const bool use_beta = (be.x != 0.0 || be.y != 0.0);
   cplx* __restrict__ Cg = P.C;
+  int emax = -2147483000;
   if (P.ksplit > 1) {
     cplx* W = P.ws + (size_t)sp * M * N;
 #pragma unroll
@@ -330,8 +337,13 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
         }
         *cp = out;
         if (mirror) Cg[rowCn[jl] + colCm[il]] = make_double2(out.x, -out.y);
+        if (P.exp_out) emax = max(emax, max(bexp(out.x), bexp(out.y)));
       }
     }
+  }
+  if (P.exp_out) {   // the tile's largest binary exponent (uniform branch)
+    for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    if (lane == 0 && emax > -2147483000) atomicMax(P.exp_out, emax);
   }
 }
 
@@ -366,6 +378,10 @@ __global__ void zgemm_splitk_reduce(const GemmProblem* __restrict__ probs, int n
       out.y += be.x * c.y + be.y * c.x;
     }
     *cp = out;
+    if (P.exp_out) {
+      const int e = max(bexp(out.x), bexp(out.y));
+      if (e > -2147483000) atomicMax(P.exp_out, e);
+    }
   }
 }
 

@@ -36,6 +36,8 @@ struct GemmProblem {
   int kchunk;          // filled by the launcher
   int tiles_mn;        // filled by the launcher: output tiles per split
   cplx* ws;            // filled by the launcher: ksplit x M x N partial products
+  int* exp_out;        // may be null: atomicMax of the binary exponents of the written C
+                       // entries (the producer side of pow2 range control)
 };
 // Device scratch for the launchers (stream-ordered bump memory owned by the caller).
 struct Scratch {
@@ -149,6 +151,10 @@ void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s);
 struct Pow2Problem { cplx* x; long long len; int* exp; };
 void launch_pow2_normalize(Pow2Problem* h, int n, Stager& st, cudaStream_t s);   // x *= 2^-e
 void launch_pow2_restore(Pow2Problem* h, int n, Stager& st, cudaStream_t s);     // x *= 2^+e
+// x *= 2^-e with *exp already holding the maximum exponent (the producing GEMM's exp_out)
+void launch_pow2_apply(Pow2Problem* h, int n, Stager& st, cudaStream_t s);
+// *exp = "no data yet" for n contiguous exponents
+void pow2_reset(int* exp, int n, cudaStream_t s);
 __host__ __device__ inline int pow2_effective(int e) { return (e < -2000 || (e > -100 && e < 100)) ? 0 : e; }
 
 // Counters of kernel launches issued by this library (for the bench's gpu_launches claim).

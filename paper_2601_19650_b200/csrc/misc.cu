@@ -210,4 +210,18 @@ void launch_pow2_restore(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
   count_launch();
 }
 
+void launch_pow2_apply(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  long long mx = 1;
+  for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].len);
+  const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
+  const unsigned gx = (unsigned)std::min<long long>((mx + 255) / 256, 296);
+  pow2_scale<<<dim3(gx, n), 256, 0, s>>>(d, -1);
+  count_launch();
+}
+
+void pow2_reset(int* exp, int n, cudaStream_t s) {
+  if (n > 0) cudaMemsetAsync(exp, 0x80, sizeof(int) * n, s);
+}
+
 }  // namespace tcbc
