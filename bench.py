@@ -418,7 +418,10 @@ def run_native(args, rank, world, local_rank):
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "peak_source": FP64_PEAK_SOURCE,
                      "flops_per_launch": g["flops"] / max(g["launches"], 1),
-                     "ms_per_launch": g["ms"] / max(g["launches"], 1)},
+                     "algorithmic_bytes_per_launch": g["bytes"] / max(g["launches"], 1),
+                     "ms_per_launch": g["ms"] / max(g["launches"], 1),
+                     "traffic_source": "profiles/ncu_zgemm_traffic_r01.json: mean DRAM read+write over every zgemm "
+                                       "launch of one config-3 step (ncu, cold-cache replays)"},
         "kernels": kern,
         "gpu_launches": int(launches),
         "clocks": clk,
