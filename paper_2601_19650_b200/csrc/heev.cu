@@ -735,6 +735,115 @@ __global__ void heev_invit(const HeevProblem* __restrict__ probs, int nprob, int
 #undef AT
 }
 
+// K3a with the working arrays in shared memory: thread = eigenvector, arrays [6][n][NT]
+// (consecutive threads in consecutive banks).  The inverse-iteration recurrences are
+// sequential per vector; with the factors and the iterate on chip every step is a shared-memory
+// access instead of an L2 round trip (the global-array version K3a stalls on L2 latency).
+constexpr int INVIT_NT = 32;
+constexpr size_t INVIT_SMEM_MAX = 200u << 10;
+
+__global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* __restrict__ probs, int nprob,
+                                                            int total, int nmax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  const int tl = threadIdx.x;
+  const int g = blockIdx.x * INVIT_NT + tl;
+  if (g >= total) return;
+  const HeevProblem& P = probs[find_estart(probs, nprob, g)];
+  const int t = g - P.estart, n = P.n, kmax = P.kmax;
+  const double* __restrict__ sd = P.work;
+  const double* __restrict__ evec = P.work + n;
+  const double* sc = P.work + 2 * n;
+  double* __restrict__ Zg = P.work + 2 * n + 8;
+  const double pert = DBL_EPSILON * sc[S_TNORM];
+  const int k = P.k_out ? *P.k_out : kmax;
+#define AR(a, i) sm[((size_t)(a) * nmax + (i)) * INVIT_NT + tl]
+  if (t >= k || !(sc[S_TNORM] > 0.0)) {   // dropped direction, or zero matrix: unit vector
+    for (int i = 0; i < n; ++i) Zg[(size_t)i * kmax + t] = (t < k && i == t) ? 1.0 : 0.0;
+    return;
+  }
+  if (cluster_arrays(P)[kmax + t] > 1.0) return;   // member of a cluster: K3b
+  enum { DL = 0, DG, DU, DU2, PV, ZZ };
+  const double lam = P.lam[t];
+  double d_i = sd[0] - lam;
+  double du_i = n > 1 ? evec[0] : 0.0;
+  for (int i = 0; i < n - 1; ++i) {   // dgttrf on T - lam I, U diagonal perturbed away from 0
+    const double dl = evec[i];
+    double d_n = sd[i + 1] - lam;
+    double du_n = (i < n - 2) ? evec[i + 1] : 0.0;
+    double du2 = 0.0, l, p = 0.0;
+    if (fabs(d_i) >= fabs(dl)) {
+      if (fabs(d_i) < pert) d_i = copysign(pert, d_i == 0.0 ? 1.0 : d_i);
+      l = dl / d_i;
+      d_n -= l * du_i;
+    } else {
+      l = d_i / dl;
+      const double old_du = du_i;
+      d_i = dl;
+      du_i = d_n;
+      du2 = du_n;
+      d_n = old_du - l * d_n;
+      du_n = -l * du_n;
+      p = 1.0;
+    }
+    if (fabs(d_i) < pert) d_i = copysign(pert, d_i == 0.0 ? 1.0 : d_i);
+    AR(DG, i) = 1.0 / d_i;
+    AR(DU, i) = du_i;
+    AR(DU2, i) = du2;
+    AR(DL, i) = l;
+    AR(PV, i) = p;
+    d_i = d_n;
+    du_i = du_n;
+  }
+  if (fabs(d_i) < pert) d_i = copysign(pert, d_i == 0.0 ? 1.0 : d_i);
+  AR(DG, n - 1) = 1.0 / d_i;
+  for (int i = 0; i < n; ++i)
+    AR(ZZ, i) = (double)(hash32((unsigned)(t * 7919 + i * 104729 + 12345)) & 0xffffff) / 16777216.0 - 0.5;
+  double scale = 1.0;
+  for (int it = 0; it < 3; ++it) {   // dgttrs, rescaled by the previous max
+    double cur = AR(ZZ, 0) * scale;
+    for (int i = 0; i < n - 1; ++i) {
+      const double nxt = AR(ZZ, i + 1) * scale;
+      const double l = AR(DL, i);
+      if (AR(PV, i) == 0.0) {
+        AR(ZZ, i) = cur;
+        cur = nxt - l * cur;
+      } else {
+        AR(ZZ, i) = nxt;
+        cur = cur - l * nxt;
+      }
+    }
+    double y2 = 0.0, y1 = cur * AR(DG, n - 1);
+    AR(ZZ, n - 1) = y1;
+    double mx = fabs(y1);
+    for (int i = n - 2; i >= 0; --i) {
+      double yi = (AR(ZZ, i) - AR(DU, i) * y1 - AR(DU2, i) * y2) * AR(DG, i);
+      if (fabs(yi) > 1e100) {   // growth through near-zero pivots: rescale the solved part
+        const double f = 1e-100;
+        for (int q = i + 1; q < n; ++q) AR(ZZ, q) *= f;
+        for (int q = 0; q < i; ++q) AR(ZZ, q) *= f;
+        yi *= f;
+        y1 *= f;
+        y2 *= f;
+        mx *= f;
+      }
+      AR(ZZ, i) = yi;
+      mx = fmax(mx, fabs(yi));
+      y2 = y1;
+      y1 = yi;
+    }
+    scale = mx > 0.0 ? 1.0 / mx : 1.0;
+  }
+  double nr = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double v = AR(ZZ, i) * scale;
+    nr += v * v;
+  }
+  const double s2 = scale / sqrt(fmax(nr, DBL_MIN));
+  for (int i = 0; i < n; ++i) Zg[(size_t)i * kmax + t] = AR(ZZ, i) * s2;
+#undef AR
+}
+
 // ---------------------------------------------------------------- K4: CholeskyQR2 of Z
 __global__ void __launch_bounds__(HEEV_THREADS) heev_orth(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
@@ -986,6 +1095,59 @@ __global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob) {
   if (P.w_out) *P.w_out = ldexp(*P.w_out, 2 * e);
 }
 
+// K5 for n <= 32 * NQ: the eigenvector lives in the warp's registers (lane l owns entries
+// l, l + 32, ...), so the sweep over the reflectors streams only v_j (independent, coalesced
+// loads) and never round-trips the vector through L2 between reflectors.
+template <int NQ>
+__global__ void heev_backtr_reg(const HeevProblem* __restrict__ probs, int nprob, int total) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (gw >= total) return;
+  const HeevProblem& P = probs[find_estart(probs, nprob, gw)];
+  const int t = gw - P.estart, n = P.n, kmax = P.kmax;
+  const double* Z = P.work + 2 * n + 8;
+  const cplx* A = P.A;
+  cplx* vt = P.Vt + (size_t)t * n;
+  const int k = P.k_out ? *P.k_out : kmax;
+  if (t >= k) {
+    for (int i = lane; i < n; i += 32) vt[i] = make_double2(0.0, 0.0);
+    return;
+  }
+  double yr[NQ], yi[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int i = lane + 32 * q;
+    yr[q] = i < n ? Z[(size_t)i * kmax + t] : 0.0;
+    yi[q] = 0.0;
+  }
+  for (int j = n - 2; j >= 0; --j) {
+    const cplx tau = P.tau[j];
+    if (tau.x == 0.0 && tau.y == 0.0) continue;
+    const cplx* row = A + (size_t)j * n;
+    cplx v[NQ];
+    double sr = 0.0, si = 0.0;   // s = v^H y over i > j
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      v[q] = (i > j && i < n) ? row[i] : make_double2(0.0, 0.0);
+      sr += v[q].x * yr[q] + v[q].y * yi[q];
+      si += v[q].x * yi[q] - v[q].y * yr[q];
+    }
+    sr = warp_sum(sr);
+    si = warp_sum(si);
+    const double tr = tau.x * sr - tau.y * si, ti = tau.x * si + tau.y * sr;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      yr[q] -= tr * v[q].x - ti * v[q].y;
+      yi[q] -= tr * v[q].y + ti * v[q].x;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int i = lane + 32 * q;
+    if (i < n) vt[i] = make_double2(yr[q], yi[q]);
+  }
+}
+
 // ---------------------------------------------------------------- K6: truncation decision
 __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1226,7 +1388,8 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   }
   const HeevProblem* d = static_cast<const HeevProblem*>(st.put(h, sizeof(HeevProblem) * n));
   prof_begin(s);
-  // K1.  Few Grams of order > 96 (chain levels): one thread-block cluster per matrix, as many
+  // K1.  Few Grams of order > 96 (chain levels; measured faster than one CTA even when the
+  // matrix fits one CTA's shared memory): one thread-block cluster per matrix, as many
   // CTAs as keep the level within ~2 waves; otherwise one CTA per matrix, one launch per
   // storage mode so small-smem problems are not limited by large ones.
   std::vector<HeevProblem> grp[3], cgrp;
@@ -1260,7 +1423,21 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   }
   heev_bisect<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
   heev_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);   // k and w: only kept pairs go on
-  heev_invit<<<(total + 127) / 128, 128, 0, s>>>(d, n, total);
+  {
+    int mxn = 1;
+    for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
+    const size_t ism = (size_t)6 * mxn * INVIT_NT * sizeof(double);
+    if (ism <= INVIT_SMEM_MAX) {
+      static bool iattr = false;
+      if (!iattr) {
+        cudaFuncSetAttribute(heev_invit_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)INVIT_SMEM_MAX);
+        iattr = true;
+      }
+      heev_invit_smem<<<(total + INVIT_NT - 1) / INVIT_NT, INVIT_NT, ism, s>>>(d, n, total, mxn);
+    } else {
+      heev_invit<<<(total + 127) / 128, 128, 0, s>>>(d, n, total);
+    }
+  }
   heev_invit_cluster<<<n, HEEV_THREADS, 0, s>>>(d);
   count_launch();
   {
@@ -1277,7 +1454,13 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
       heev_orth<<<n, HEEV_THREADS, 0, s>>>(d);
     }
   }
-  heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+  {
+    int mxn = 0;
+    for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
+    if (mxn <= 128) heev_backtr_reg<4><<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+    else if (mxn <= 256) heev_backtr_reg<8><<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+    else heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+  }
   heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n);
   count_launch();
   count_launch(); count_launch(); count_launch(); count_launch(); count_launch();
