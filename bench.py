@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-showcase", action="store_true", help="skip the config-4 FP64 roofline sidecar")
     ap.add_argument("--workers", type=int, default=None, help="concurrent sub-batches (ttn_ctx_set_workers)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="short run for ncu: no e2e/cpu/clocks")
@@ -211,6 +212,47 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- native arm
+def config4_showcase(ctx, stream, steps=3):
+    """Sidecar of the default (config 3) line: BASELINE config 4, the FP64-bound workload
+    (2048 x 16384 x 2048 contractions, n = 2048 Grams), timed the same way on the same GPU, so
+    the line also shows the dominant kernel where the contractions are large."""
+    import torch
+    import paper_2601_19650_b200 as P
+    inst = W.make_config(4, seed=0)
+    st = P.ttn_create(ctx, P.TTN_STATE, inst.parent, inst.phys, inst.state_bond, inst.state)
+    nrm = P.ttn_norm(ctx, st)
+    tens = [t.copy() for t in inst.state]
+    tens[0] = tens[0] / nrm
+    st.destroy()
+    st = P.ttn_create(ctx, P.TTN_STATE, inst.parent, inst.phys, inst.state_bond, tens)
+    op = P.ttn_create(ctx, P.TTN_OPERATOR, inst.parent, inst.phys, inst.op_bond, inst.op)
+    out, _ = P.cbc_apply(ctx, op, st, inst.max_bond)   # warm-up
+    out.destroy()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=torch.cuda.current_device())
+    P.ttn_profile_enable(True)
+    ms, fl = 0.0, 0.0
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out, rep = P.cbc_apply(ctx, op, st, inst.max_bond)
+        e1.record(stream)
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+        fl += rep["flops_algorithmic"]
+        out.destroy()
+    g = P.ttn_profile_read("zgemm")
+    P.ttn_profile_enable(False)
+    st.destroy()
+    op.destroy()
+    ach = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
+    return {"workload": workload_desc(4, 1)["workload"], "applies_per_s": steps / (ms / 1e3),
+            "ms_per_apply": ms / steps, "fp64_tflops_end_to_end": fl / (ms / 1e3) / 1e12,
+            "roofline": {"bound": "tensor", "kernel": "zgemm_grouped (DMMA.8x8x4 complex GEMM)", "achieved": ach,
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS},
+            "note": "timed after the main line, same GPU and clocks, L2 flushed between applies"}
+
+
 def run_native(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -383,6 +425,9 @@ def run_native(args, rank, world, local_rank):
             "value": None, "unit": "applies/s", "cores": blas_threads(), "kind": "oracle",
             "sample": "not re-timed by default: one config-4 oracle apply takes ~350 s on 8 cores "
                       "(tests/golden/cfg4_seed0.json oracle_seconds), beyond the bench's few-minute budget"}
+    showcase = None
+    if world == 1 and cfg == 3 and not args.quick and not args.no_showcase:
+        showcase = config4_showcase(ctx, stream)
     g = prof["zgemm"]
     ach = g["flops"] / (g["ms"] / 1000.0) / 1e12 if g["ms"] > 0 else 0.0
     traffic = None
@@ -427,6 +472,7 @@ def run_native(args, rank, world, local_rank):
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "fp64_showcase": showcase,
     }
     print(json.dumps(line), flush=True)
     ctx.close()
