@@ -739,15 +739,15 @@ __global__ void heev_invit(const HeevProblem* __restrict__ probs, int nprob, int
 // (consecutive threads in consecutive banks).  The inverse-iteration recurrences are
 // sequential per vector; with the factors and the iterate on chip every step is a shared-memory
 // access instead of an L2 round trip (the global-array version K3a stalls on L2 latency).
-constexpr int INVIT_NT = 32;
+constexpr int INVIT_NT = 32;   // max vectors per block (fewer when 6 n NT doubles exceed the budget)
 constexpr size_t INVIT_SMEM_MAX = 200u << 10;
 
 __global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* __restrict__ probs, int nprob,
                                                             int total, int nmax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
-  const int tl = threadIdx.x;
-  const int g = blockIdx.x * INVIT_NT + tl;
+  const int tl = threadIdx.x, NT = blockDim.x;
+  const int g = blockIdx.x * NT + tl;
   if (g >= total) return;
   const HeevProblem& P = probs[find_estart(probs, nprob, g)];
   const int t = g - P.estart, n = P.n, kmax = P.kmax;
@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* _
   double* __restrict__ Zg = P.work + 2 * n + 8;
   const double pert = DBL_EPSILON * sc[S_TNORM];
   const int k = P.k_out ? *P.k_out : kmax;
-#define AR(a, i) sm[((size_t)(a) * nmax + (i)) * INVIT_NT + tl]
+#define AR(a, i) sm[((size_t)(a) * nmax + (i)) * NT + tl]
   if (t >= k || !(sc[S_TNORM] > 0.0)) {   // dropped direction, or zero matrix: unit vector
     for (int i = 0; i < n; ++i) Zg[(size_t)i * kmax + t] = (t < k && i == t) ? 1.0 : 0.0;
     return;
@@ -1426,14 +1426,16 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   {
     int mxn = 1;
     for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
-    const size_t ism = (size_t)6 * mxn * INVIT_NT * sizeof(double);
+    int nt = INVIT_NT;
+    while (nt > 8 && (size_t)6 * mxn * nt * sizeof(double) > INVIT_SMEM_MAX) nt /= 2;
+    const size_t ism = (size_t)6 * mxn * nt * sizeof(double);
     if (ism <= INVIT_SMEM_MAX) {
       static bool iattr = false;
       if (!iattr) {
         cudaFuncSetAttribute(heev_invit_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)INVIT_SMEM_MAX);
         iattr = true;
       }
-      heev_invit_smem<<<(total + INVIT_NT - 1) / INVIT_NT, INVIT_NT, ism, s>>>(d, n, total, mxn);
+      heev_invit_smem<<<(total + nt - 1) / nt, nt, ism, s>>>(d, n, total, mxn);
     } else {
       heev_invit<<<(total + 127) / 128, 128, 0, s>>>(d, n, total);
     }
