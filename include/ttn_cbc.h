@@ -62,6 +62,9 @@ typedef struct {
   double flops_algorithmic;    /* 8 * complex MACs of every contraction / Gram / factor GEMM */
   int32_t rank_fallbacks;      /* Eq. 13 QRs that fell back from CholeskyQR2 (rank-deficient) */
   int32_t host_syncs;          /* stream synchronisations taken for data-dependent ranks     */
+  int32_t split_compresses;    /* partitioned apply: compresses whose Gram was row-split over
+                                  ranks (partial Grams summed by allreduce); 0 otherwise      */
+  int32_t reserved;
 } ttn_cbc_report;
 
 /* ---------------------------------------------------------------- context             */

@@ -32,7 +32,8 @@ class c128(C.Structure):
 class Report(C.Structure):
     _fields_ = [("norm", C.c_double), ("discarded_weight_sum", C.c_double), ("max_bond", C.c_int64),
                 ("peak_entries", C.c_int64), ("seconds", C.c_double), ("flops_algorithmic", C.c_double),
-                ("rank_fallbacks", C.c_int32), ("host_syncs", C.c_int32)]
+                ("rank_fallbacks", C.c_int32), ("host_syncs", C.c_int32), ("split_compresses", C.c_int32),
+                ("reserved", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

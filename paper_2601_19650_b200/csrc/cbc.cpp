@@ -42,6 +42,7 @@ struct CompressJob {
   int64_t a, b;      // column legs of X (n = a*b)
   int inst;
   int* exp = nullptr;   // max binary exponent of X, written by the producing GEMM (or null)
+  cplx* G_pre = nullptr;   // row-split compress: the (already range-scaled) Gram X^H X; G route only
 };
 
 struct QRJob {
@@ -108,12 +109,17 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     const int64_t kmax = std::min<int64_t>(max_bond, nn);
     if (!chfsi_applicable((int)std::min<int64_t>(nn, INT32_MAX), (int)kmax)) check_heev_size(nn);
     kmaxs[j] = kmax;
-    cplx* G = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
-    GemmProblem g = (m >= n) ? mk_gemm(J.X, OP_C, n, J.X, OP_N, n, G, nn, n, n, m)     // G = X^H X
-                             : mk_gemm(J.X, OP_N, n, J.X, OP_C, n, G, nn, m, m, n);    // K = X X^H
-    g.sym = 1;   // Hermitian: lower tiles + mirror (HERK)
-    grams.push_back(g);
-    flops_inst[J.inst] += gemm_flops(g);
+    cplx* G = J.G_pre;
+    if (!G) {
+      G = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
+      GemmProblem g = (m >= n) ? mk_gemm(J.X, OP_C, n, J.X, OP_N, n, G, nn, n, n, m)     // G = X^H X
+                               : mk_gemm(J.X, OP_N, n, J.X, OP_C, n, G, nn, m, m, n);    // K = X X^H
+      g.sym = 1;   // Hermitian: lower tiles + mirror (HERK)
+      grams.push_back(g);
+      flops_inst[J.inst] += gemm_flops(g);
+    } else if (m < n) {
+      throw Error(TTN_ERR_ARG, "row-split compress needs the G route (m >= n)");
+    }
     HeevProblem& h = hp[j];
     h.A = G;
     h.n = (int)nn;
@@ -146,13 +152,17 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     st.peak_entries = std::max(st.peak_entries, nn * nn);
   }
   {   // the Gram squares X: exponents from the producing GEMM's epilogue where available
-    std::vector<Pow2Problem> have, need;
-    for (int j = 0; j < nj; ++j) (jobs[j].exp ? have : need).push_back(p2[j]);
+    std::vector<Pow2Problem> have, need, back;
+    for (int j = 0; j < nj; ++j) {
+      if (jobs[j].G_pre) continue;   // row-split: X was scaled before its partial Grams
+      (jobs[j].exp ? have : need).push_back(p2[j]);
+      back.push_back(p2[j]);
+    }
     launch_pow2_apply(have.data(), (int)have.size(), *ctx->stager, ctx->stream);
     launch_pow2_normalize(need.data(), (int)need.size(), *ctx->stager, ctx->stream);
+    gemm_batch(ctx, grams, st);
+    launch_pow2_restore(back.data(), (int)back.size(), *ctx->stager, ctx->stream);   // the K-route factor reads X
   }
-  gemm_batch(ctx, grams, st);
-  launch_pow2_restore(p2.data(), nj, *ctx->stager, ctx->stream);     // the K-route factor reads X
   static const bool dump = getenv("TTN_DEBUG_HEEV") && std::string(getenv("TTN_DEBUG_HEEV")) == "3";
   std::vector<std::vector<cplx>> gcopy;
   if (dump) {   // debug: keep the Grams (heev destroys them) to dump the ones that fail
@@ -410,7 +420,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   // per-instance accumulators: replicated top work counted on every rank, subtree work only
   // on its owner (summed over ranks at the end)
   std::vector<double> w_inst(nb, 0.0), flops_inst(nb, 0.0), w_sub(nb, 0.0), flops_sub(nb, 0.0);
-  std::vector<int> fb_inst(nb, 0), fb_sub(nb, 0);
+  std::vector<int> fb_inst(nb, 0), fb_sub(nb, 0), split_inst(nb, 0);
   std::vector<Fac> up((size_t)nb * n), down((size_t)nb * n), R((size_t)nb * n);
   // trivial factor L^{[(-,r)]} = 1 (extent-1 legs)
   cplx* one = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx)));
@@ -419,6 +429,107 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
 
   auto acc_w = [&](bool sub) -> std::vector<double>& { return sub ? w_sub : w_inst; };
   auto acc_f = [&](bool sub) -> std::vector<double>& { return sub ? flops_sub : flops_inst; };
+
+  // ---------------- row split of the replicated top's heavy compresses (partitioned apply):
+  // a G-route compress of X (rows m >= cols n) whose widest factor leg has extent k is cut into
+  // S >= world slices along that leg; each rank contracts its slices X_s (the factor operand
+  // is a contiguous sub-block), forms sum_s X_s^H X_s, and the partial Grams are summed over
+  // ranks (ncclAllReduce) -- G = X^H X exactly, at 1/world of the contraction and Gram work.
+  // The eigensolve and the factor (Lambda^1/2 V^H needs only G) then run replicated.
+  // TTN_PARTITION_SLICES (tests) forces more slices than ranks on one GPU.
+  const char* slices_env = getenv("TTN_PARTITION_SLICES");
+  const int nslices = part.on ? std::max(part.world, slices_env ? atoi(slices_env) : 0) : 1;
+  const int64_t split_min = slices_env ? 0 : (int64_t(1) << 22);   // entries of X worth splitting
+  auto split_rows = [&](std::vector<Task>& tasks, std::vector<CompressJob>& jobs) {
+    if (nslices < 2) return;
+    std::vector<Task> keep_t, sl_t;
+    std::vector<CompressJob> keep_j, sp_j;
+    std::vector<int> sl_job, sl_s;
+    for (size_t j = 0; j < tasks.size(); ++j) {
+      Task& t = tasks[j];
+      CompressJob& J = jobs[j];
+      const int64_t n = J.a * J.b;
+      int64_t m = t.ops[1].dims[0];   // sigma'
+      for (size_t o = 2; o < t.ops.size(); ++o) m *= t.ops[o].dims[0];
+      size_t fo = 0;   // slice the factor with the widest compressed leg
+      for (size_t o = 2; o < t.ops.size(); ++o)
+        if (!fo || t.ops[o].dims[0] > t.ops[fo].dims[0]) fo = o;
+      const int64_t k = fo ? t.ops[fo].dims[0] : 1;
+      if (m < n || k < nslices || m * n < split_min) {   // K route, too thin, or small: replicated
+        keep_t.push_back(t);
+        keep_j.push_back(J);
+        continue;
+      }
+      for (int sl = 0; sl < nslices; ++sl) {
+        if (sl % part.world != part.rank) continue;
+        const int64_t k0 = k * sl / nslices, k1 = k * (sl + 1) / nslices;
+        Task ts = t;
+        Operand& F = ts.ops[fo];
+        F.ptr += k0 * F.dims[1] * F.dims[2];
+        F.dims[0] = k1 - k0;
+        ts.out = nullptr;
+        sl_t.push_back(ts);
+        sl_job.push_back((int)sp_j.size());
+        sl_s.push_back(sl);
+      }
+      J.m = m;
+      J.n = n;
+      ++split_inst[J.inst];
+      sp_j.push_back(J);
+    }
+    tasks.swap(keep_t);
+    jobs.swap(keep_j);
+    if (sp_j.empty()) return;
+    // shared range exponent per job (max over slices and ranks), then the partial Grams
+    const int ns = (int)sp_j.size();
+    int* d_e = static_cast<int*>(ctx->env.alloc(sizeof(int) * ns));
+    pow2_reset(d_e, ns, ctx->stream);
+    for (size_t q = 0; q < sl_t.size(); ++q) sl_t[q].out_exp = d_e + sl_job[q];
+    ExecStats cs;
+    if (!sl_t.empty()) contract_batch(ctx, sl_t, cs);
+    for (size_t q = 0; q < sl_t.size(); ++q) flops_sub[sp_j[sl_job[q]].inst] += sl_t[q].flops;
+    st.flops += cs.flops;
+    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+    comm->allreduce_max(d_e, ns, ctx->stream);
+    std::vector<Pow2Problem> p2;
+    for (size_t q = 0; q < sl_t.size(); ++q) {
+      int64_t tot = 1;
+      for (auto d : sl_t[q].out_dims) tot *= d;
+      p2.push_back(Pow2Problem{sl_t[q].out, tot, d_e + sl_job[q]});
+    }
+    launch_pow2_apply(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
+    std::vector<cplx*> G(ns);
+    for (int q = 0; q < ns; ++q) {
+      const int64_t n = sp_j[q].n;
+      G[q] = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * n * n));
+      TTN_CUDA(cudaMemsetAsync(G[q], 0, sizeof(cplx) * n * n, ctx->stream));
+    }
+    // rounds of one slice per job (beta = 1 accumulation keeps the rounds stream-ordered)
+    for (int round = 0;; ++round) {
+      std::vector<GemmProblem> g;
+      std::vector<int> seen(ns, 0);
+      for (size_t q = 0; q < sl_t.size(); ++q) {
+        const int jq = sl_job[q];
+        if (seen[jq]++ != round) continue;
+        const int64_t n = sp_j[jq].n;
+        int64_t tot = 1;
+        for (auto d : sl_t[q].out_dims) tot *= d;
+        GemmProblem gp = mk_gemm(sl_t[q].out, OP_C, n, sl_t[q].out, OP_N, n, G[jq], n, n, n, tot / n);
+        gp.beta = make_double2(1.0, 0.0);
+        flops_sub[sp_j[jq].inst] += gemm_flops(gp);
+        g.push_back(gp);
+      }
+      if (g.empty()) break;
+      gemm_batch(ctx, g, st);
+    }
+    for (int q = 0; q < ns; ++q) comm->allreduce_sum(reinterpret_cast<double*>(G[q]), 2 * (size_t)sp_j[q].n * sp_j[q].n, ctx->stream);
+    for (int q = 0; q < ns; ++q) {
+      sp_j[q].G_pre = G[q];
+      sp_j[q].exp = d_e + q;
+      sp_j[q].X = nullptr;
+    }
+    compress_batch(ctx, sp_j, max_bond, tol, st, w_inst, flops_inst);
+  };
 
   // ---------------- 1. up-sweep (Eq. 10) over the nodes selected by `sel`, deepest level first
   auto up_sweep = [&](auto sel, bool sub) {
@@ -434,6 +545,8 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
           jobs.push_back(CompressJob{nullptr, 0, 0, &up[(size_t)b * n + i], sts[b]->shape[i][1], ops[b]->shape[i][2], b});
         }
       if (tasks.empty()) continue;
+      if (!sub && part.on) split_rows(tasks, jobs);   // heavy replicated G-route compresses
+      if (tasks.empty()) { ctx->scratch.reset(); continue; }
       int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * tasks.size()));
       pow2_reset(d_e, (int)tasks.size(), ctx->stream);
       for (size_t j = 0; j < tasks.size(); ++j) {
@@ -475,6 +588,8 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
           }
         }
       if (tasks.empty()) continue;
+      if (!sub && part.on) split_rows(tasks, jobs);   // heavy replicated G-route compresses
+      if (tasks.empty()) { ctx->scratch.reset(); continue; }
       int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * tasks.size()));
       pow2_reset(d_e, (int)tasks.size(), ctx->stream);
       for (size_t j = 0; j < tasks.size(); ++j) {
@@ -700,6 +815,8 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       r.flops_algorithmic = flops_inst[b];
       r.rank_fallbacks = fb_inst[b];
       r.host_syncs = ctx->host_syncs;
+      r.split_compresses = split_inst[b];
+      r.reserved = 0;
     }
   }
 }

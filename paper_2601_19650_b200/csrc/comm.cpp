@@ -15,7 +15,7 @@ typedef int nres_t;   // ncclResult_t
 typedef void* ncomm_t;
 struct NcclId { char internal[128]; };
 enum { nccl_int32 = 2, nccl_float64 = 8 };   // ncclDataType_t
-enum { nccl_sum = 0 };                         // ncclRedOp_t
+enum { nccl_sum = 0, nccl_max = 2 };           // ncclRedOp_t
 
 struct Nccl {
   void* h = nullptr;
@@ -97,6 +97,11 @@ void Comm::allreduce_sum(double* buf, size_t n, cudaStream_t s) {
 void Comm::allreduce_sum(int* buf, size_t n, cudaStream_t s) {
   if (!comm || n == 0) return;
   check(nccl().AllReduce(buf, buf, n, nccl_int32, nccl_sum, comm, s), "ncclAllReduce");
+}
+
+void Comm::allreduce_max(int* buf, size_t n, cudaStream_t s) {
+  if (!comm || n == 0) return;
+  check(nccl().AllReduce(buf, buf, n, nccl_int32, nccl_max, comm, s), "ncclAllReduce");
 }
 
 void Comm::group_start() {

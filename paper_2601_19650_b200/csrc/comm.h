@@ -16,6 +16,7 @@ struct Comm {
   // in-place sum of `n` doubles / int32s
   void allreduce_sum(double* buf, size_t n, cudaStream_t s);
   void allreduce_sum(int* buf, size_t n, cudaStream_t s);
+  void allreduce_max(int* buf, size_t n, cudaStream_t s);
   void group_start();
   void group_end();
   ~Comm();

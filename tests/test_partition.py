@@ -98,8 +98,14 @@ def test_two_gloo_ranks_agree_on_id_plan_and_split():
 @pytest.mark.gpu
 @pytest.mark.parametrize("tree,chi,D,mb", [("binary31", 4, 3, 6), ("star3x2", 3, 2, 4), ("binary63", 3, 2, 4)])
 @pytest.mark.parametrize("parts", [2, 4])
-def test_partitioned_schedule_matches_plain_apply(tree, chi, D, mb, parts):
+@pytest.mark.parametrize("slices", [None, 3])
+def test_partitioned_schedule_matches_plain_apply(tree, chi, D, mb, parts, slices, monkeypatch):
+    """slices=3: the top's G-route compresses are row-split into 3 virtual slices (the
+    multi-GPU path of cbc.cpp split_rows with every slice on this rank), so sum_s X_s^H X_s
+    must reproduce the plain Gram X^H X."""
     import torch
+    if slices is not None:
+        monkeypatch.setenv("TTN_PARTITION_SLICES", str(slices))
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2601_19650_b200 as P
@@ -123,13 +129,18 @@ def test_partitioned_schedule_matches_plain_apply(tree, chi, D, mb, parts):
         assert d_cos <= 1e-14, (d_cos, d_rel)
         assert abs(rep1["discarded_weight_sum"] - rep0["discarded_weight_sum"]) <= 1e-12 * max(1.0, rep0["discarded_weight_sum"])
         assert abs(rep1["norm"] - rep0["norm"]) <= 1e-12 * rep0["norm"]
+        assert rep0["split_compresses"] == 0
+        assert (rep1["split_compresses"] > 0) == (slices is not None)
     finally:
         ctx.close()
 
 
 @pytest.mark.gpu
-def test_partitioned_config4_matches_golden():
+@pytest.mark.parametrize("slices", [None, 4])
+def test_partitioned_config4_matches_golden(slices, monkeypatch):
     import json
+    if slices is not None:
+        monkeypatch.setenv("TTN_PARTITION_SLICES", str(slices))
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -147,6 +158,7 @@ def test_partitioned_config4_matches_golden():
         phi = to_oracle(P, out, inst.parent)
         assert phi.bonds() == gold["bonds"]
         assert abs(norm(phi) ** 2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"]
+        assert (rep["split_compresses"] > 0) == (slices is not None)
     finally:
         ctx.close()
 
