@@ -10,13 +10,14 @@
 //              tridiagonal; the complex reflector makes every off-diagonal real).  n <= 256:
 //              lower triangle only, rank-2 update of step j-1 fused into the Hermitian mat-vec
 //              of step j (one pass per step), the packed triangle in shared memory for n <= 144.
-//  K2 bisect   one thread per (matrix, eigenvalue): Sturm-count quartersection (3 interleaved
-//              chains hide the division latency) for the top kmax eigenvalues.
+//  K2 bisect   G lanes per (matrix, eigenvalue): Sturm-count multisection for the top kmax
+//              eigenvalues (G sized to the level).
 //  K3 invit    one thread per (matrix, eigenvector): inverse iteration on T - lam I
 //              (dgttrf / dgttrs with partial pivoting), scratch interleaved across threads.
 //  K4 orth     one CTA per matrix: CholeskyQR2 of the kmax vectors (clusters of close
 //              eigenvalues leave inverse-iteration vectors only approximately orthogonal).
-//  K5 backtr   one warp per (matrix, eigenvector): V = Q Z by the stored reflectors.
+//  K5 backtr   one warp per (matrix, eigenvector): V = Q Z by the stored reflectors, staged
+//              through shared memory by a CTA of 8 eigenvectors of the same matrix.
 //  K6 finish   truncation decision k = min(max_bond, #{lam > tol^2 lam_1}, #{lam > floor lam_1})
 //              >= 1 and discarded weight w = trace(A) - sum_{t<k} lam_t.
 #include "kernels.h"
@@ -586,14 +587,19 @@ __device__ __forceinline__ double frcp(double b) {
   return r;
 }
 
-// One warp per (matrix, eigenvalue): multisection.  Each lane evaluates Sturm counts at two
-// of 64 interior points of [lo, hi] (two interleaved chains hide the division latency); the
-// interval shrinks 65x per round, so ~9 rounds reach the dstebz tolerance instead of ~50
-// bisection steps.  Counts are exact integers, so the result is the same bracket bisection
-// would converge to.
+// G lanes per (matrix, eigenvalue): multisection.  Each lane evaluates Sturm counts at two of
+// the 2G interior points of [lo, hi] (two interleaved chains hide the division latency); the
+// interval shrinks (2G+1)x per round.  Counts are exact integers, so the result is the same
+// bracket bisection would converge to.  G trades rounds (latency) for Sturm evaluations
+// (FP64 work): the launcher takes the smallest G that still fills the GPU (config 3's
+// 16384-eigenvalue levels: G = 4, ~17 rounds of 8 points, instead of 9 rounds of 64).
+template <int G>
 __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, int total) {
-  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (g >= total) return;
+  const int lane = threadIdx.x & 31, sub = lane % G;
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if ((blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / G >= total) return;   // whole warp idle
+  const int g = min(g0, total - 1);                 // tail lanes shadow the last eigenvalue
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane - sub));
   const HeevProblem& P = probs[find_estart(probs, nprob, g)];
   const int t = g - P.estart, n = P.n;
   const double* d = P.work;
@@ -602,10 +608,11 @@ __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, in
   const double pivmin = sc[S_PIVMIN], atol = sc[S_ATOL];
   const int idx = n - 1 - t;                   // ascending index of the t-th largest
   double lo = sc[S_GL], hi = sc[S_GU];
-  for (int it = 0; it < 40; ++it) {
-    if (hi - lo <= fmax(atol, 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) + pivmin) break;
-    const double w = (hi - lo) / 65.0;
-    const double x1 = lo + w * (2 * lane + 1), x2 = lo + w * (2 * lane + 2);
+  for (int it = 0; it < 96; ++it) {
+    const bool done = hi - lo <= fmax(atol, 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) + pivmin;
+    if (__all_sync(0xffffffffu, done)) break;
+    const double w = (hi - lo) / (2 * G + 1);
+    const double x1 = lo + w * (2 * sub + 1), x2 = lo + w * (2 * sub + 2);
     int c1 = 0, c2 = 0;
     double q1 = d[0] - x1, q2 = d[0] - x2;
     if (q1 <= pivmin) { ++c1; q1 = fmin(q1, -pivmin); }
@@ -618,17 +625,20 @@ __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, in
       if (q2 <= pivmin) { ++c2; q2 = fmin(q2, -pivmin); }
     }
     // the eigenvalue lies in the first sub-interval whose right end has count > idx
-    const unsigned b1 = __ballot_sync(0xffffffffu, c1 > idx), b2 = __ballot_sync(0xffffffffu, c2 > idx);
-    // point index p = 2*lane + (0 | 1); first p with count > idx
-    int pfirst = 64;
+    const unsigned b1 = (__ballot_sync(0xffffffffu, c1 > idx) & gmask) >> (lane - sub);
+    const unsigned b2 = (__ballot_sync(0xffffffffu, c2 > idx) & gmask) >> (lane - sub);
+    // point index p = 2*sub + (0 | 1); first p with count > idx
+    int pfirst = 2 * G;
     if (b1) pfirst = min(pfirst, 2 * (__ffs(b1) - 1));
     if (b2) pfirst = min(pfirst, 2 * (__ffs(b2) - 1) + 1);
-    const double nlo = pfirst == 0 ? lo : lo + w * pfirst;
-    const double nhi = pfirst == 64 ? hi : lo + w * (pfirst + 1);
-    lo = nlo;
-    hi = nhi;
+    if (!done) {
+      const double nlo = pfirst == 0 ? lo : lo + w * pfirst;
+      const double nhi = pfirst == 2 * G ? hi : lo + w * (pfirst + 1);
+      lo = nlo;
+      hi = nhi;
+    }
   }
-  if (lane == 0) P.lam[t] = 0.5 * (lo + hi);
+  if (sub == 0 && g0 < total) P.lam[t] = 0.5 * (lo + hi);
 }
 
 // ---------------------------------------------------------------- K3: inverse iteration
@@ -1095,52 +1105,82 @@ __global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob) {
   if (P.w_out) *P.w_out = ldexp(*P.w_out, 2 * e);
 }
 
-// K5 for n <= 32 * NQ: the eigenvector lives in the warp's registers (lane l owns entries
-// l, l + 32, ...), so the sweep over the reflectors streams only v_j (independent, coalesced
-// loads) and never round-trips the vector through L2 between reflectors.
+// K5 for n <= 32 * NQ, one CTA per (matrix, 8 eigenvectors): the eigenvector lives in its
+// warp's registers (lane l owns entries l, l + 32, ...); the reflectors are staged BT_R rows at
+// a time in shared memory by the whole CTA (one coalesced L2 pass shared by 8 vectors), so the
+// sequential sweep reads v_j from shared memory instead of waiting on L2 per reflector.
+constexpr int BT_WARPS = 8, BT_R = 16;
+__host__ __device__ inline size_t backtr_smem_bytes(int n) { return (size_t)BT_R * n * 16 + BT_R * 16; }
+
+__device__ __forceinline__ int find_bstart(const HeevProblem* p, int n, int b) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p[mid].bstart <= b) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 template <int NQ>
-__global__ void heev_backtr_reg(const HeevProblem* __restrict__ probs, int nprob, int total) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (gw >= total) return;
-  const HeevProblem& P = probs[find_estart(probs, nprob, gw)];
-  const int t = gw - P.estart, n = P.n, kmax = P.kmax;
+__global__ void __launch_bounds__(BT_WARPS * 32) heev_backtr_blk(const HeevProblem* __restrict__ probs, int nprob) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const HeevProblem& P = probs[find_bstart(probs, nprob, blockIdx.x)];
+  const int t0 = (blockIdx.x - P.bstart) * BT_WARPS, t = t0 + warp, n = P.n, kmax = P.kmax;
+  cplx* sv = reinterpret_cast<cplx*>(smem_raw);
+  cplx* stau = sv + (size_t)BT_R * n;
   const double* Z = P.work + 2 * n + 8;
   const cplx* A = P.A;
   cplx* vt = P.Vt + (size_t)t * n;
   const int k = P.k_out ? *P.k_out : kmax;
-  if (t >= k) {
-    for (int i = lane; i < n; i += 32) vt[i] = make_double2(0.0, 0.0);
+  if (t0 >= k) {   // block-uniform: every vector of this block is dropped
+    if (t < kmax)
+      for (int i = lane; i < n; i += 32) vt[i] = make_double2(0.0, 0.0);
     return;
   }
+  const bool act = t < k;
   double yr[NQ], yi[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int i = lane + 32 * q;
-    yr[q] = i < n ? Z[(size_t)i * kmax + t] : 0.0;
+    yr[q] = (act && i < n) ? Z[(size_t)i * kmax + t] : 0.0;
     yi[q] = 0.0;
   }
-  for (int j = n - 2; j >= 0; --j) {
-    const cplx tau = P.tau[j];
-    if (tau.x == 0.0 && tau.y == 0.0) continue;
-    const cplx* row = A + (size_t)j * n;
-    cplx v[NQ];
-    double sr = 0.0, si = 0.0;   // s = v^H y over i > j
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int i = lane + 32 * q;
-      v[q] = (i > j && i < n) ? row[i] : make_double2(0.0, 0.0);
-      sr += v[q].x * yr[q] + v[q].y * yi[q];
-      si += v[q].x * yi[q] - v[q].y * yr[q];
+  for (int j1 = n - 2; j1 >= 0; j1 -= BT_R) {
+    const int j0 = max(0, j1 - BT_R + 1);
+    __syncthreads();
+    for (int r = warp; r <= j1 - j0; r += BT_WARPS) {
+      const int j = j0 + r;
+      const cplx* row = A + (size_t)j * n;
+      for (int i = lane; i < n; i += 32) sv[(size_t)r * n + i] = i > j ? row[i] : make_double2(0.0, 0.0);
     }
-    sr = warp_sum(sr);
-    si = warp_sum(si);
-    const double tr = tau.x * sr - tau.y * si, ti = tau.x * si + tau.y * sr;
+    if ((int)threadIdx.x <= j1 - j0) stau[threadIdx.x] = P.tau[j0 + threadIdx.x];
+    __syncthreads();
+    if (!act) continue;
+    for (int j = j1; j >= j0; --j) {
+      const cplx tau = stau[j - j0];
+      if (tau.x == 0.0 && tau.y == 0.0) continue;
+      const cplx* row = sv + (size_t)(j - j0) * n;
+      cplx v[NQ];
+      double sr = 0.0, si = 0.0;   // s = v^H y over i > j (entries i <= j are staged as 0)
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      yr[q] -= tr * v[q].x - ti * v[q].y;
-      yi[q] -= tr * v[q].y + ti * v[q].x;
+      for (int q = 0; q < NQ; ++q) {
+        const int i = lane + 32 * q;
+        v[q] = i < n ? row[i] : make_double2(0.0, 0.0);
+        sr += v[q].x * yr[q] + v[q].y * yi[q];
+        si += v[q].x * yi[q] - v[q].y * yr[q];
+      }
+      sr = warp_sum(sr);
+      si = warp_sum(si);
+      const double tr = tau.x * sr - tau.y * si, ti = tau.x * si + tau.y * sr;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        yr[q] -= tr * v[q].x - ti * v[q].y;
+        yi[q] -= tr * v[q].y + ti * v[q].x;
+      }
     }
   }
+  if (t >= kmax) return;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int i = lane + 32 * q;
@@ -1379,9 +1419,12 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   }
   int total = 0;
   double fl = 0.0, by = 0.0;
+  int nblk = 0;
   for (int i = 0; i < n; ++i) {
     h[i].estart = total;
     total += h[i].kmax;
+    h[i].bstart = nblk;
+    nblk += (h[i].kmax + BT_WARPS - 1) / BT_WARPS;
     const double nn = h[i].n;
     fl += 8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * h[i].kmax);
     by += 16.0 * nn * nn;
@@ -1421,7 +1464,19 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
     heev_tridiag<<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
     count_launch();
   }
-  heev_bisect<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+  {   // smallest lanes-per-eigenvalue that still keeps ~12 warps per SM busy
+    int G = 1;
+    while (G < 32 && (long long)total * G < 148LL * 12 * 32) G *= 2;
+    const int blocks = (int)(((long long)total * G + 255) / 256);
+    switch (G) {
+      case 1: heev_bisect<1><<<blocks, 256, 0, s>>>(d, n, total); break;
+      case 2: heev_bisect<2><<<blocks, 256, 0, s>>>(d, n, total); break;
+      case 4: heev_bisect<4><<<blocks, 256, 0, s>>>(d, n, total); break;
+      case 8: heev_bisect<8><<<blocks, 256, 0, s>>>(d, n, total); break;
+      case 16: heev_bisect<16><<<blocks, 256, 0, s>>>(d, n, total); break;
+      default: heev_bisect<32><<<blocks, 256, 0, s>>>(d, n, total); break;
+    }
+  }
   heev_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);   // k and w: only kept pairs go on
   {
     int mxn = 1;
@@ -1459,9 +1514,18 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   {
     int mxn = 0;
     for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
-    if (mxn <= 128) heev_backtr_reg<4><<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
-    else if (mxn <= 256) heev_backtr_reg<8><<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
-    else heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+    if (mxn <= 256) {
+      static bool battr = false;
+      if (!battr) {
+        cudaFuncSetAttribute(heev_backtr_blk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
+        cudaFuncSetAttribute(heev_backtr_blk<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
+        battr = true;
+      }
+      if (mxn <= 128) heev_backtr_blk<4><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
+      else heev_backtr_blk<8><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
+    } else {
+      heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+    }
   }
   heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n);
   count_launch();

@@ -79,6 +79,7 @@ struct HeevProblem {
   double floor_rel;    // rank floor on lam / lam_1
   int max_bond;
   int estart;          // filled by the launcher: prefix sum of kmax (eigenpair task index)
+  int bstart;          // filled by the launcher: first back-transform block of this problem
   const int* exp2;     // may be null: A was formed from data scaled by 2^-e (pow2_normalize);
                        // the returned eigenvalues and discarded weight are scaled by 2^(2e)
 };
