@@ -41,8 +41,8 @@ struct Cfg {
   static constexpr int LDAK = BM + 2, LDBK = BN + 2;
   static constexpr int A_ELEMS = AKM ? BK * LDAK : BM * PADK;
   static constexpr int B_ELEMS = BNM ? BN * PADK : BK * LDBK;
-  static constexpr int TAB = (3 * BM + 3 * BN + 2 * STAGES * BK) * 8;
-  static constexpr int BYTES = STAGES * (A_ELEMS + B_ELEMS) * 16 + TAB + 1024;
+  static constexpr int TAB = (2 * (3 * BM + 3 * BN) + 2 * STAGES * BK) * 8;
+  static constexpr int BYTES = STAGES * (A_ELEMS + B_ELEMS) * 16 + TAB + 2 * (int)sizeof(GemmProblem) + 64;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -95,92 +95,127 @@ __device__ __forceinline__ int find_problem(const GemmProblem* p, int n, int til
   return lo;
 }
 
+// Persistent: CTA c takes tiles c, c + gridDim.x, ...  Each tile's operand tables (row / column
+// offsets, problem descriptor) are double-buffered in shared memory, so the next tile is set up
+// and its first STAGES-1 operand stages are in flight (cp.async) while this tile's epilogue
+// stores its accumulators: the prologue latency of short-K tiles (config 3's K = 32 steps)
+// hides behind the epilogue instead of idling the tensor pipe.
 template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
-__global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob) {
+__global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob,
+                                                            int total_tiles) {
   using C_ = Cfg<BM, BN, AKM, BNM>;
   constexpr int WTM = BM / WGM, WTN = BN / WGN;     // warp tile
   constexpr int TM = WTM / 8, TN = WTN / 8;         // DMMA tiles per warp
+  constexpr int TABN = 3 * BM + 3 * BN;             // offsets per table buffer
+  constexpr int PWORDS = (int)(sizeof(GemmProblem) / 8);
+  static_assert(sizeof(GemmProblem) % 8 == 0, "descriptor copy");
   static_assert(WGM * WGN == THREADS / 32, "warp grid");
   static_assert((BM * BK) % THREADS == 0 && (BN * BK) % THREADS == 0, "load mapping");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
   cplx* Bs = As + STAGES * C_::A_ELEMS;
-  long long* rowA = reinterpret_cast<long long*>(Bs + STAGES * C_::B_ELEMS);
-  long long* colB = rowA + BM;
-  long long* rowC = colB + BN;
-  long long* colC = rowC + BM;
-  long long* colCm = colC + BN;              // sym: column offsets of the m indices (mirror)
-  long long* rowCn = colCm + BM;             // sym: row offsets of the n indices (mirror)
-  long long* kA = rowCn + BN;                // [STAGES][BK] k-leg offsets into A (-1: k >= K)
+  long long* tab = reinterpret_cast<long long*>(Bs + STAGES * C_::B_ELEMS);   // [2][TABN]
+  long long* kA = tab + 2 * TABN;            // [STAGES][BK] k-leg offsets into A (-1: k >= K)
   long long* kB = kA + STAGES * BK;          // [STAGES][BK] k-leg offsets into B
-  GemmProblem* sP = reinterpret_cast<GemmProblem*>(kB + STAGES * BK);
+  GemmProblem* sP = reinterpret_cast<GemmProblem*>(kB + STAGES * BK);   // [2]
+  int* sPi = reinterpret_cast<int*>(sP + 2);                            // [2] problem index
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) *sP = probs[find_problem(probs, nprob, blockIdx.x)];
-  __syncthreads();
-  const GemmProblem& P = *sP;
-  const int t0 = blockIdx.x - P.tile_start;
-  const int sp = t0 / P.tiles_mn, t = t0 % P.tiles_mn;   // k split, output tile
-  int bi, bj;
-  if (P.sym) {   // lower-triangular tile index
-    bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-    while (bi * (bi + 1) / 2 > t) --bi;
-    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-    bj = t - bi * (bi + 1) / 2;
-  } else {
-    bi = t / P.tiles_n;
-    bj = t % P.tiles_n;
-  }
-  const int m0 = bi * BM, n0 = bj * BN;
-  const bool mirror = P.sym && bi != bj;
-  const int M = P.M, N = P.N;
-  const int kbeg = sp * P.kchunk, K = min(P.K, kbeg + P.kchunk);   // this CTA's k range [kbeg, K)
-  for (int i = tid; i < BM; i += THREADS) {
-    const int m = m0 + i;
-    rowA[i] = m < M ? goff(m, P.nm, P.md, P.am) : -1;
-    rowC[i] = m < M ? goff(m, P.nm, P.md, P.cm) : -1;
-    if (mirror) colCm[i] = m < M ? goff(m, P.nn, P.nd, P.cn) : -1;
-  }
-  for (int i = tid; i < BN; i += THREADS) {
-    const int n = n0 + i;
-    colB[i] = n < N ? goff(n, P.nn, P.nd, P.bn) : -1;
-    colC[i] = n < N ? goff(n, P.nn, P.nd, P.cn) : -1;
-    if (mirror) rowCn[i] = n < N ? goff(n, P.nm, P.md, P.cm) : -1;
-  }
-  const int ktiles = (K - kbeg + BK - 1) / BK;
-  // k-leg offsets of tile T into ring slot T % STAGES (thread j < 2*BK: operand j / BK, k j % BK)
-  auto k_offsets = [&](int T, int j) {
-    const int slot = T % STAGES, kl = j % BK, k = kbeg + T * BK + kl;
-    if (j < BK) kA[slot * BK + kl] = k < K ? goff(k, P.nk, P.kd, P.ak) : -1;
-    else kB[slot * BK + kl] = k < K ? goff(k, P.nk, P.kd, P.bk) : -1;
-  };
-  if (P.nk != 1)
-    for (int j = tid; j < 2 * BK * STAGES; j += THREADS) {
-      const int T = j / (2 * BK);
-      if (T < ktiles) k_offsets(T, j % (2 * BK));
-    }
-  __syncthreads();
-  const cplx* __restrict__ Ag = P.A;
-  const cplx* __restrict__ Bg = P.B;
   const int wm = (warp / WGN) * WTM, wn = (warp % WGN) * WTN;
-  const bool conjA = P.conjA != 0, conjB = P.conjB != 0;
+  const int fr = lane >> 2, fc = lane & 3;   // fragment row / col within 8x4 / 4x8
 
-  const bool k1 = P.nk == 1;               // single k leg: offsets are k * stride, no ring
-  const long long ak0 = P.ak[0], bk0 = P.bk[0];
-  auto kofs = [&](const long long* ring, long long st0, int T, int kl) -> long long {
-    if (k1) {
-      const int k = kbeg + T * BK + kl;
-      return k < K ? (long long)k * st0 : -1;
+  struct Tile { int m0, n0, sp, kbeg, K, ktiles; bool mirror; };
+  // descriptor + tables + first k-ring entries of `tile` into buffer `buf` (all threads)
+  auto prepare = [&](int tile, int buf, int prev) -> Tile {
+    if (tid == 0) {
+      int pi = -1;
+      if (prev >= 0) {   // consecutive tiles mostly belong to the same problem
+        const GemmProblem& Q = sP[prev];
+        if (tile >= Q.tile_start && tile < Q.tile_start + Q.tiles_mn * Q.ksplit) pi = sPi[prev];
+      }
+      sPi[buf] = pi >= 0 ? pi : find_problem(probs, nprob, tile);
     }
-    return ring[(T % STAGES) * BK + kl];
+    __syncthreads();
+    {
+      const long long* src = reinterpret_cast<const long long*>(probs + sPi[buf]);
+      long long* dst = reinterpret_cast<long long*>(sP + buf);
+      for (int i = tid; i < PWORDS; i += THREADS) dst[i] = src[i];
+    }
+    __syncthreads();
+    const GemmProblem& P = sP[buf];
+    const int t0 = tile - P.tile_start;
+    const int sp = t0 / P.tiles_mn, t = t0 % P.tiles_mn;   // k split, output tile
+    int bi, bj;
+    if (P.sym) {   // lower-triangular tile index
+      bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+      while (bi * (bi + 1) / 2 > t) --bi;
+      while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+      bj = t - bi * (bi + 1) / 2;
+    } else {
+      bi = t / P.tiles_n;
+      bj = t % P.tiles_n;
+    }
+    Tile T;
+    T.m0 = bi * BM;
+    T.n0 = bj * BN;
+    T.sp = sp;
+    T.mirror = P.sym && bi != bj;
+    T.kbeg = sp * P.kchunk;
+    T.K = min(P.K, T.kbeg + P.kchunk);   // this tile's k range [kbeg, K)
+    T.ktiles = (T.K - T.kbeg + BK - 1) / BK;
+    long long* rowA = tab + buf * TABN;
+    long long* colB = rowA + BM;
+    long long* rowC = colB + BN;
+    long long* colC = rowC + BM;
+    long long* colCm = colC + BN;
+    long long* rowCn = colCm + BM;
+    for (int i = tid; i < BM; i += THREADS) {
+      const int m = T.m0 + i;
+      rowA[i] = m < P.M ? goff(m, P.nm, P.md, P.am) : -1;
+      rowC[i] = m < P.M ? goff(m, P.nm, P.md, P.cm) : -1;
+      if (T.mirror) colCm[i] = m < P.M ? goff(m, P.nn, P.nd, P.cn) : -1;
+    }
+    for (int i = tid; i < BN; i += THREADS) {
+      const int n = T.n0 + i;
+      colB[i] = n < P.N ? goff(n, P.nn, P.nd, P.bn) : -1;
+      colC[i] = n < P.N ? goff(n, P.nn, P.nd, P.cn) : -1;
+      if (T.mirror) rowCn[i] = n < P.N ? goff(n, P.nm, P.md, P.cm) : -1;
+    }
+    if (P.nk != 1)
+      for (int j = tid; j < 2 * BK * STAGES; j += THREADS) {
+        const int Tk = j / (2 * BK), jj = j % (2 * BK);
+        if (Tk < T.ktiles) {
+          const int kl = jj % BK, k = T.kbeg + Tk * BK + kl;
+          if (jj < BK) kA[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.ak) : -1;
+          else kB[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.bk) : -1;
+        }
+      }
+    __syncthreads();
+    return T;
   };
-  auto load_stage = [&](int T) {
-    const int stage = T % STAGES;
+
+  // operand stage Tk of tile T (buffer buf) into ring slot Tk % STAGES
+  auto load_stage = [&](const Tile& T, int buf, int Tk) {
+    const GemmProblem& P = sP[buf];
+    const long long* rowA = tab + buf * TABN;
+    const long long* colB = rowA + BM;
+    const bool k1 = P.nk == 1;
+    const long long ak0 = P.ak[0], bk0 = P.bk[0];
+    auto kofs = [&](const long long* ring, long long st0, int kl) -> long long {
+      if (k1) {
+        const int k = T.kbeg + Tk * BK + kl;
+        return k < T.K ? (long long)k * st0 : -1;
+      }
+      return ring[(Tk % STAGES) * BK + kl];
+    };
+    const cplx* __restrict__ Ag = P.A;
+    const cplx* __restrict__ Bg = P.B;
+    const int stage = Tk % STAGES;
     cplx* as = As + stage * C_::A_ELEMS;
     cplx* bs = Bs + stage * C_::B_ELEMS;
     if (!AKM) {   // As[m][k]: k fixed per thread
       const int k = tid % BK;
-      const long long ko = kofs(kA, ak0, T, k);
+      const long long ko = kofs(kA, ak0, k);
 #pragma unroll
       for (int r = 0; r < (BM * BK) / THREADS; ++r) {
         const int m = tid / BK + r * (THREADS / BK);
@@ -193,14 +228,14 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
       for (int r = 0; r < (BM * BK) / THREADS; ++r) {
         const int idx = tid + r * THREADS;
         const int k = idx / BM, m = idx % BM;
-        const long long ro = rowA[m], ko = kofs(kA, ak0, T, k);
+        const long long ro = rowA[m], ko = kofs(kA, ak0, k);
         const bool v = ko >= 0 && ro >= 0;
         cp_async16(as + k * C_::LDAK + m, v ? Ag + ro + ko : Ag, v);
       }
     }
     if (BNM) {    // Bs[n][k]: k fixed per thread
       const int k = tid % BK;
-      const long long ko = kofs(kB, bk0, T, k);
+      const long long ko = kofs(kB, bk0, k);
 #pragma unroll
       for (int r = 0; r < (BN * BK) / THREADS; ++r) {
         const int n = tid / BK + r * (THREADS / BK);
@@ -213,138 +248,171 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
       for (int r = 0; r < (BN * BK) / THREADS; ++r) {
         const int idx = tid + r * THREADS;
         const int k = idx / BN, n = idx % BN;
-        const long long co = colB[n], ko = kofs(kB, bk0, T, k);
+        const long long co = colB[n], ko = kofs(kB, bk0, k);
         const bool v = ko >= 0 && co >= 0;
         cp_async16(bs + k * C_::LDBK + n, v ? Bg + co + ko : Bg, v);
       }
     }
   };
-
-  double acc_re[TM][TN][2], acc_im[TM][TN][2];
+  auto prologue = [&](const Tile& T, int buf) {
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
-      acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-    }
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_stage(s);
-    cp_async_commit();
-  }
-
-  const int fr = lane >> 2, fc = lane & 3;   // fragment row / col within 8x4 / 4x8
-  for (int kt = 0; kt < ktiles; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    // decode the k legs of tile kt + STAGES (slot kt % STAGES: its last reader, the load of
-    // tile kt, was issued before this barrier); visible to the loads after the next barrier
-    if (!k1 && tid < 2 * BK && kt + STAGES < ktiles) k_offsets(kt + STAGES, tid);
-    {
-      const int kn = kt + STAGES - 1;
-      if (kn < ktiles) load_stage(kn);
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < T.ktiles) load_stage(T, buf, s);
       cp_async_commit();
     }
-    const cplx* as = As + (kt % STAGES) * C_::A_ELEMS;
-    const cplx* bs = Bs + (kt % STAGES) * C_::B_ELEMS;
-    double ar[BK / 4][TM], ai[BK / 4][TM], nai[BK / 4][TM], br[BK / 4][TN], bi[BK / 4][TN];
+  };
+
+  int tile = blockIdx.x;
+  if (tile >= total_tiles) return;
+  int buf = 0;
+  Tile T = prepare(tile, 0, -1);
+  prologue(T, 0);
+  while (true) {
+    const GemmProblem& P = sP[buf];
+    const bool conjA = P.conjA != 0, conjB = P.conjB != 0;
+    double acc_re[TM][TN][2], acc_im[TM][TN][2];
 #pragma unroll
-    for (int q = 0; q < BK / 4; ++q) {
-      const int k = q * 4 + fc;
-#pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const int m = wm + i * 8 + fr;
-        const cplx a = AKM ? as[k * C_::LDAK + m] : as[m * PADK + k];
-        ar[q][i] = a.x;
-        ai[q][i] = neg_if(a.y, conjA);
-        nai[q][i] = neg_if(a.y, !conjA);
-      }
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
-        const int n = wn + j * 8 + fr;
-        const cplx b = BNM ? bs[n * PADK + k] : bs[k * C_::LDBK + n];
-        br[q][j] = b.x;
-        bi[q][j] = neg_if(b.y, conjB);
+        acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
+        acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+      }
+    for (int kt = 0; kt < T.ktiles; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      // decode the k legs of tile kt + STAGES (slot kt % STAGES: its last reader, the load of
+      // tile kt, was issued before this barrier); visible to the loads after the next barrier
+      if (P.nk != 1 && tid < 2 * BK && kt + STAGES < T.ktiles) {
+        const int Tk = kt + STAGES, kl = tid % BK, k = T.kbeg + Tk * BK + kl;
+        if (tid < BK) kA[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.ak) : -1;
+        else kB[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.bk) : -1;
+      }
+      {
+        const int kn = kt + STAGES - 1;
+        if (kn < T.ktiles) load_stage(T, buf, kn);
+        cp_async_commit();
+      }
+      const cplx* as = As + (kt % STAGES) * C_::A_ELEMS;
+      const cplx* bs = Bs + (kt % STAGES) * C_::B_ELEMS;
+      double ar[BK / 4][TM], ai[BK / 4][TM], nai[BK / 4][TM], br[BK / 4][TN], bi[BK / 4][TN];
+#pragma unroll
+      for (int q = 0; q < BK / 4; ++q) {
+        const int k = q * 4 + fc;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const int m = wm + i * 8 + fr;
+          const cplx a = AKM ? as[k * C_::LDAK + m] : as[m * PADK + k];
+          ar[q][i] = a.x;
+          ai[q][i] = neg_if(a.y, conjA);
+          nai[q][i] = neg_if(a.y, !conjA);
+        }
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const int n = wn + j * 8 + fr;
+          const cplx b = BNM ? bs[n * PADK + k] : bs[k * C_::LDBK + n];
+          br[q][j] = b.x;
+          bi[q][j] = neg_if(b.y, conjB);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < BK / 4; ++q) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], ar[q][i], br[q][j]);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], ar[q][i], bi[q][j]);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], nai[q][i], bi[q][j]);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], ai[q][i], br[q][j]);
       }
     }
-#pragma unroll
-    for (int q = 0; q < BK / 4; ++q) {
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], ar[q][i], br[q][j]);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], ar[q][i], bi[q][j]);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], nai[q][i], bi[q][j]);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], ai[q][i], br[q][j]);
+    // every warp is done with this tile's stages and k ring: set up the next tile and start
+    // its loads, then store this one
+    const int next = tile + gridDim.x;
+    const bool more = next < total_tiles;
+    __syncthreads();
+    Tile Tn{};
+    if (more) {
+      Tn = prepare(next, buf ^ 1, buf);
+      prologue(Tn, buf ^ 1);
     }
+
+    // epilogue: C = alpha * acc + beta * C (strided store: the output permutation is fused here);
+    // split-k partials go raw to the workspace; Hermitian products also write the mirror tile
+    {
+      const long long* rowC = tab + buf * TABN + BM + BN;
+      const long long* colC = rowC + BM;
+      const long long* colCm = colC + BN;
+      const long long* rowCn = colCm + BM;
+      const int M = P.M, N = P.N;
+      const cplx al = P.alpha, be = P.beta;
+      const bool use_beta = (be.x != 0.0 || be.y != 0.0);
+      cplx* __restrict__ Cg = P.C;
+      int emax = -2147483000;
+      if (P.ksplit > 1) {
+        cplx* W = P.ws + (size_t)T.sp * M * N;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const int m = T.m0 + wm + i * 8 + fr;
+          if (m >= M) continue;
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int n = T.n0 + wn + j * 8 + fc * 2 + h;
+              if (n < N) W[(size_t)m * N + n] = make_double2(acc_re[i][j][h], acc_im[i][j][h]);
+            }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const int il = wm + i * 8 + fr;
+          const long long ro = rowC[il];
+          if (ro < 0) continue;
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int jl = wn + j * 8 + fc * 2 + h;
+              const long long co = colC[jl];
+              if (co < 0) continue;
+              const double re = acc_re[i][j][h], im = acc_im[i][j][h];
+              cplx out;
+              out.x = al.x * re - al.y * im;
+              out.y = al.x * im + al.y * re;
+              cplx* cp = Cg + ro + co;
+              if (use_beta) {
+                const cplx c = *cp;
+                out.x += be.x * c.x - be.y * c.y;
+                out.y += be.x * c.y + be.y * c.x;
+              }
+              *cp = out;
+              if (T.mirror) Cg[rowCn[jl] + colCm[il]] = make_double2(out.x, -out.y);
+              if (P.exp_out) emax = max(emax, max(bexp(out.x), bexp(out.y)));
+            }
+          }
+        }
+        if (P.exp_out) {   // the tile's largest binary exponent (uniform branch)
+          for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+          if (lane == 0 && emax > -2147483000) atomicMax(P.exp_out, emax);
+        }
+      }
+    }
+    if (!more) break;
+    tile = next;
+    buf ^= 1;
+    T = Tn;
   }
   cp_async_wait<0>();
-
-  // epilogue: C = alpha * acc + beta * C (strided store: the output permutation is fused here);
-  // split-k partials go raw to the workspace; Hermitian products also write the mirror tile
-  const cplx al = P.alpha, be = P.beta;
-  const bool use_beta = (be.x != 0.0 || be.y != 0.0);
-  cplx* __restrict__ Cg = P.C;
-  int emax = -2147483000;
-  if (P.ksplit > 1) {
-    cplx* W = P.ws + (size_t)sp * M * N;
-#pragma unroll
-    for (int i = 0; i < TM; ++i) {
-      const int m = m0 + wm + i * 8 + fr;
-      if (m >= M) continue;
-#pragma unroll
-      for (int j = 0; j < TN; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int n = n0 + wn + j * 8 + fc * 2 + h;
-          if (n < N) W[(size_t)m * N + n] = make_double2(acc_re[i][j][h], acc_im[i][j][h]);
-        }
-    }
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const int il = wm + i * 8 + fr;
-    const long long ro = rowC[il];
-    if (ro < 0) continue;
-#pragma unroll
-    for (int j = 0; j < TN; ++j) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jl = wn + j * 8 + fc * 2 + h;
-        const long long co = colC[jl];
-        if (co < 0) continue;
-        const double re = acc_re[i][j][h], im = acc_im[i][j][h];
-        cplx out;
-        out.x = al.x * re - al.y * im;
-        out.y = al.x * im + al.y * re;
-        cplx* cp = Cg + ro + co;
-        if (use_beta) {
-          const cplx c = *cp;
-          out.x += be.x * c.x - be.y * c.y;
-          out.y += be.x * c.y + be.y * c.x;
-        }
-        *cp = out;
-        if (mirror) Cg[rowCn[jl] + colCm[il]] = make_double2(out.x, -out.y);
-        if (P.exp_out) emax = max(emax, max(bexp(out.x), bexp(out.y)));
-      }
-    }
-  }
-  if (P.exp_out) {   // the tile's largest binary exponent (uniform branch)
-    for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-    if (lane == 0 && emax > -2147483000) atomicMax(P.exp_out, emax);
-  }
 }
 
 // split-k reduction: C = alpha * sum_s W_s + beta * C (C through its strided legs)
@@ -408,8 +476,9 @@ void launch_variant(std::vector<GemmProblem>& h, Stager& st, cudaStream_t s) {
                          C_::BYTES);
     attr_done = true;
   }
+  const int grid = std::min(tiles, 2 * 148);   // persistent: two resident CTAs per SM
   prof_begin(s);
-  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM><<<tiles, THREADS, C_::BYTES, s>>>(d, (int)h.size());
+  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM><<<grid, THREADS, C_::BYTES, s>>>(d, (int)h.size(), tiles);
   prof_end(s, "zgemm", flops, bytes);
   count_launch();
 }
