@@ -118,12 +118,16 @@ PlanT make_plan(const Task& t) {
     for (int l : L) p *= (double)dim[l];
     return p;
   };
-  // cost of a pairwise step: time at the FP64 roofline (37 TF/s, 6.5 TB/s)
+  // cost of a pairwise step: time at the FP64 roofline (37 TF/s, 6.5 TB/s), the DMMA rate
+  // derated for short contractions: a tile's fixed prologue / epilogue costs about 24 k-steps
+  // (measured, tools/gemm_bench: 19 TF/s at K = 32, 29 at K = 128, 34 at K = 4096)
+  static const double k0 = getenv("TTN_PLAN_K0") ? atof(getenv("TTN_PLAN_K0")) : 24.0;
   auto step_cost = [&](int sa, int sb, int sm) {
     std::vector<int> un = freel[sa];
     for (int l : freel[sb])
       if (std::find(un.begin(), un.end(), l) == un.end()) un.push_back(l);
-    const double fl = 8.0 * prod(un);
+    const double kk = prod(un) / std::max(1.0, prod(freel[sm]));   // contracted extent
+    const double fl = 8.0 * prod(un) * (1.0 + k0 / std::max(1.0, kk));
     const double by = 16.0 * (prod(freel[sa]) + prod(freel[sb]) + prod(freel[sm]));
     return std::max(fl / 37e12, by / 6.5e12) + 2e-7;
   };
