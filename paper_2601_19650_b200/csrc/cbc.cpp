@@ -12,6 +12,7 @@
 #include "chfsi.h"
 #include "contract.h"
 #include "runtime.h"
+#include "prof.h"
 
 #include <algorithm>
 #include <chrono>
@@ -94,6 +95,7 @@ void check_heev_size(int64_t nn) {
 void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_bond, double tol,
                     ExecStats& st, std::vector<double>& w_inst, std::vector<double>& flops_inst) {
   if (jobs.empty()) return;
+  HostScope hs_("compress_batch");
   const int nj = (int)jobs.size();
   std::vector<GemmProblem> grams, fgemm;
   std::vector<HeevProblem> hp(nj);
@@ -233,6 +235,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
 int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vector<double>& flops_inst,
              std::vector<int>& fb_inst) {
   if (jobs.empty()) return 0;
+  HostScope hs_("qr_batch");
   std::vector<EyeProblem> eyes;
   std::vector<GemmProblem> g1, g2, g3, g4;
   std::vector<PotrfProblem> p1, p2;
@@ -416,6 +419,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   ctx->env.reset();
   ctx->scratch.reset();
   ctx->host_syncs = 0;
+  ctx->sync_wait_s = 0.0;
   ExecStats st;
   // per-instance accumulators: replicated top work counted on every rank, subtree work only
   // on its owner (summed over ranks at the end)
@@ -533,7 +537,9 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
 
   // ---------------- 1. up-sweep (Eq. 10) over the nodes selected by `sel`, deepest level first
   auto up_sweep = [&](auto sel, bool sub) {
+    HostScope hs_("up_sweep");
     for (int L = maxd; L >= 1; --L) {
+      HostScope hb_("build_tasks");
       std::vector<Task> tasks;
       std::vector<CompressJob> jobs;
       for (int b = 0; b < nb; ++b)
@@ -571,6 +577,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   };
   // ---------------- 2. down-sweep (Eq. 11): nodes selected by `sel` give their children factors
   auto down_sweep = [&](auto sel, bool sub) {
+    HostScope hs_("down_sweep");
     for (int L = 0; L < maxd; ++L) {
       std::vector<Task> tasks;
       std::vector<CompressJob> jobs;
@@ -691,6 +698,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
 
   // ---------------- 3. final sweep (Eqs. 12-14) and 4. assembly, over the nodes selected
   auto final_sweep = [&](auto sel, bool sub) {
+    HostScope hs_("final_sweep");
     for (int L = maxd; L >= 0; --L) {
       std::vector<Task> tasks;
       std::vector<std::pair<int, int>> who;
@@ -803,6 +811,13 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   for (int b = 0; b < nb; ++b)
     if (!std::isfinite(hs[b])) throw Error(TTN_ERR_NUMERIC, "non-finite result (non-finite input?)");
   double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  static const bool hprof = getenv("TTN_HOST_PROF") != nullptr;
+  if (hprof) {
+    fprintf(stderr, "[host] apply %.3f ms: blocked in %d syncs %.3f ms, host work %.3f ms\n", secs * 1e3,
+            ctx->host_syncs, ctx->sync_wait_s * 1e3, (secs - ctx->sync_wait_s) * 1e3);
+    host_prof_add("sync_wait", ctx->sync_wait_s);
+    host_prof_dump();
+  }
   if (reps) {
     for (int b = 0; b < nb; ++b) {
       ttn_cbc_report& r = reps[b];

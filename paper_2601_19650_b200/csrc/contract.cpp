@@ -6,6 +6,7 @@
 // so executing a batch is: bump-allocate the intermediates, patch pointers, and issue one
 // grouped GEMM launch per step round.
 #include "contract.h"
+#include "prof.h"
 
 #include <algorithm>
 #include <cmath>
@@ -270,6 +271,7 @@ double gemm_flops(const GemmProblem& g) {
 }
 
 void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st) {
+  HostScope hs_("gemm_batch");
   for (auto& g : probs) st.flops += gemm_flops(g);
   static const bool dbg = getenv("TTN_DEBUG_GEMM") != nullptr;
   if (dbg && !probs.empty()) {
@@ -303,6 +305,7 @@ GemmProblem mk_gemm(const cplx* A, int opA, long long lda, const cplx* B, int op
 }
 
 void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st) {
+  HostScope hs_("contract_batch");
   if (tasks.empty()) return;
   static const bool dbg0 = getenv("TTN_DEBUG_CONTRACT") != nullptr;
   if (dbg0) {   // debug: inputs must be finite before any launch of this batch

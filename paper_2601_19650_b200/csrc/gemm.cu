@@ -453,12 +453,12 @@ __global__ void zgemm_splitk_reduce(const GemmProblem* __restrict__ probs, int n
   }
 }
 
-template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
-void launch_variant(std::vector<GemmProblem>& h, Stager& st, cudaStream_t s) {
-  if (h.empty()) return;
+// tile bookkeeping of one variant's problems (tile_start, tiles_n, tiles_mn); returns the tiles
+template <int BM, int BN>
+int assign_tiles(GemmProblem* h, int n, double& flops, double& bytes) {
   int tiles = 0;
-  double flops = 0.0, bytes = 0.0;
-  for (auto& p : h) {
+  for (int i = 0; i < n; ++i) {
+    GemmProblem& p = h[i];
     const int tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
     p.tile_start = tiles;
     p.tiles_n = std::max(tn, 1);
@@ -467,8 +467,12 @@ void launch_variant(std::vector<GemmProblem>& h, Stager& st, cudaStream_t s) {
     flops += p.sym ? 8.0 * 0.5 * (double)p.M * (p.M + 1) * p.K : 8.0 * (double)p.M * p.N * p.K;
     bytes += 16.0 * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N);
   }
-  if (tiles == 0) return;
-  const GemmProblem* d = static_cast<const GemmProblem*>(st.put(h.data(), sizeof(GemmProblem) * h.size()));
+  return tiles;
+}
+
+template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
+void launch_variant(const GemmProblem* d, int n, int tiles, cudaStream_t s) {
+  if (n == 0 || tiles == 0) return;
   using C_ = Cfg<BM, BN, AKM, BNM>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -477,18 +481,8 @@ void launch_variant(std::vector<GemmProblem>& h, Stager& st, cudaStream_t s) {
     attr_done = true;
   }
   const int grid = std::min(tiles, 2 * 148);   // persistent: two resident CTAs per SM
-  prof_begin(s);
-  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM><<<grid, THREADS, C_::BYTES, s>>>(d, (int)h.size(), tiles);
-  prof_end(s, "zgemm", flops, bytes);
+  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM><<<grid, THREADS, C_::BYTES, s>>>(d, n, tiles);
   count_launch();
-}
-
-template <int BM, int BN, int WGM, int WGN>
-void launch_shape(std::vector<GemmProblem>* g4, Stager& st, cudaStream_t s) {
-  launch_variant<BM, BN, WGM, WGN, false, false>(g4[0], st, s);
-  launch_variant<BM, BN, WGM, WGN, false, true>(g4[1], st, s);
-  launch_variant<BM, BN, WGM, WGN, true, false>(g4[2], st, s);
-  launch_variant<BM, BN, WGM, WGN, true, true>(g4[3], st, s);
 }
 
 // CTA tile shapes (BM x BN); warp tiles 32x32 except the 16-wide skinny shapes (32x16, 16x32)
@@ -520,11 +514,18 @@ void gemm_from_ops(GemmProblem& g, int opA, long long lda, int opB, long long ld
 }
 
 void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws) {
+  HostScope hs_("launch_gemm");
   // group by tile shape (least padded work) and shared-memory layouts; Hermitian products take
   // the square tile (lower-triangle tiles only); problems that cannot fill the GPU with output
-  // tiles get their k range split (deterministic: partials reduced in a second kernel)
-  std::vector<GemmProblem> by[kNumShapes][4];
-  std::vector<GemmProblem> split;
+  // tiles get their k range split (deterministic: partials reduced in a second kernel).  All
+  // groups go to the device in one staging copy and are timed as one zgemm launch set.
+  constexpr int NV = kNumShapes * 4;
+  thread_local std::vector<GemmProblem> all;
+  thread_local std::vector<int> grp;
+  all.clear();
+  grp.clear();
+  int cnt[NV] = {0};
+  int nsplit = 0;
   for (int i = 0; i < n; ++i) {
     GemmProblem p = h[i];
     if (p.M <= 0 || p.N <= 0) continue;
@@ -557,24 +558,64 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
           p.ksplit = S;
           p.kchunk = chunk;
           p.ws = static_cast<cplx*>(ws->get(sizeof(cplx) * (size_t)S * p.M * p.N));
+          ++nsplit;
         }
       }
     }
-    by[best][v].push_back(p);
-    if (p.ksplit > 1) split.push_back(p);
+    const int g = best * 4 + v;
+    ++cnt[g];
+    grp.push_back(g);
+    all.push_back(p);
   }
-  launch_shape<64, 64, 2, 2>(by[0], st, s);
-  launch_shape<128, 32, 4, 1>(by[1], st, s);
-  launch_shape<32, 128, 1, 4>(by[2], st, s);
-  launch_shape<128, 16, 4, 1>(by[3], st, s);
-  launch_shape<16, 128, 1, 4>(by[4], st, s);
-  if (!split.empty()) {
-    const GemmProblem* d = static_cast<const GemmProblem*>(st.put(split.data(), sizeof(GemmProblem) * split.size()));
+  if (all.empty()) return;
+  // order by group (stable), then the split-k problems again for the reduction kernel
+  int off[NV + 1];
+  off[0] = 0;
+  for (int g = 0; g < NV; ++g) off[g + 1] = off[g] + cnt[g];
+  const int total = (int)all.size();
+  thread_local std::vector<GemmProblem> ord;
+  ord.resize((size_t)total + nsplit);
+  {
+    int pos[NV];
+    for (int g = 0; g < NV; ++g) pos[g] = off[g];
+    int sp = total;
+    for (int i = 0; i < total; ++i) {
+      ord[pos[grp[i]]++] = all[i];
+      if (all[i].ksplit > 1) ord[sp++] = all[i];
+    }
+  }
+  double flops = 0.0, bytes = 0.0;
+  int tiles[NV];
+  for (int g = 0; g < NV; ++g) {
+    GemmProblem* q = ord.data() + off[g];
+    switch (g / 4) {
+      case 0: tiles[g] = assign_tiles<64, 64>(q, cnt[g], flops, bytes); break;
+      case 1: tiles[g] = assign_tiles<128, 32>(q, cnt[g], flops, bytes); break;
+      case 2: tiles[g] = assign_tiles<32, 128>(q, cnt[g], flops, bytes); break;
+      case 3: tiles[g] = assign_tiles<128, 16>(q, cnt[g], flops, bytes); break;
+      default: tiles[g] = assign_tiles<16, 128>(q, cnt[g], flops, bytes); break;
+    }
+  }
+  const GemmProblem* d = static_cast<const GemmProblem*>(st.put(ord.data(), sizeof(GemmProblem) * ord.size()));
+#define TCBC_LV(G, BM, BN, WM, WN)                                                             \
+  launch_variant<BM, BN, WM, WN, false, false>(d + off[G + 0], cnt[G + 0], tiles[G + 0], s); \
+  launch_variant<BM, BN, WM, WN, false, true>(d + off[G + 1], cnt[G + 1], tiles[G + 1], s);  \
+  launch_variant<BM, BN, WM, WN, true, false>(d + off[G + 2], cnt[G + 2], tiles[G + 2], s);  \
+  launch_variant<BM, BN, WM, WN, true, true>(d + off[G + 3], cnt[G + 3], tiles[G + 3], s);
+  prof_begin(s);
+  TCBC_LV(0, 64, 64, 2, 2)
+  TCBC_LV(4, 128, 32, 4, 1)
+  TCBC_LV(8, 32, 128, 1, 4)
+  TCBC_LV(12, 128, 16, 4, 1)
+  TCBC_LV(16, 16, 128, 1, 4)
+#undef TCBC_LV
+  prof_end(s, "zgemm", flops, bytes);
+  if (nsplit > 0) {
     long long mx = 0;
-    for (auto& p : split) mx = std::max<long long>(mx, (long long)p.M * p.N);
+    for (int i = total; i < total + nsplit; ++i) mx = std::max<long long>(mx, (long long)ord[i].M * ord[i].N);
     const int gx = (int)std::min<long long>((mx + 255) / 256, 1024);
     prof_begin(s);
-    zgemm_splitk_reduce<<<dim3(gx, (unsigned)split.size()), 256, 0, s>>>(d, (int)split.size());
+    zgemm_splitk_reduce<<<dim3(gx, (unsigned)nsplit), 256, 0, s>>>(d + total, nsplit);
     prof_end(s, "zgemm_reduce", 0.0, 0.0);
     count_launch();
   }

@@ -1411,6 +1411,7 @@ void launch_tridiag_cluster(const HeevProblem* d, int nprob, int cs, size_t smem
 }  // namespace
 
 void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
+  HostScope hs_("launch_heev");
   if (n == 0) return;
   static bool attr = false;
   if (!attr) {

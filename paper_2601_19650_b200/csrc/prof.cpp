@@ -1,3 +1,6 @@
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include "prof.h"
 
 #include <map>
@@ -113,4 +116,36 @@ bool prof_read(const char* family, double* ms, double* flops, double* bytes, lon
   return true;
 }
 
+}  // namespace tcbc
+
+namespace tcbc {
+namespace {
+std::mutex g_hmu;
+std::map<std::string, double>& hmap() {
+  static std::map<std::string, double> m;
+  return m;
+}
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+thread_local double t_wait = 0.0;
+void host_prof_wait(double seconds) { t_wait += seconds; }
+bool host_prof_on() {
+  static const bool on = getenv("TTN_HOST_PROF") != nullptr;
+  return on;
+}
+void host_prof_add(const char* name, double seconds) {
+  std::lock_guard<std::mutex> lk(g_hmu);
+  hmap()[name] += seconds;
+}
+void host_prof_dump() {
+  std::lock_guard<std::mutex> lk(g_hmu);
+  for (auto& kv : hmap()) fprintf(stderr, "  [host] %-18s %8.3f ms\n", kv.first.c_str(), kv.second * 1e3);
+  hmap().clear();
+}
+HostScope::HostScope(const char* n) : name(n), t0(host_prof_on() ? now_s() : 0.0), w0(t_wait) {}
+HostScope::~HostScope() {
+  if (host_prof_on()) host_prof_add(name, now_s() - t0 - (t_wait - w0));
+}
 }  // namespace tcbc

@@ -11,4 +11,17 @@ void prof_end(cudaStream_t s, const char* family, double flops, double bytes);
 void prof_enable(bool on);
 bool prof_read(const char* family, double* ms, double* flops, double* bytes, long long* launches);
 
+// Host wall-time accumulators (TTN_HOST_PROF diagnostics; no-ops otherwise).  Nested scopes
+// double count; host_prof_dump prints and clears.
+bool host_prof_on();
+void host_prof_add(const char* name, double seconds);
+void host_prof_dump();
+void host_prof_wait(double seconds);   // time blocked in stream synchronisation (excluded)
+struct HostScope {
+  const char* name;
+  double t0, w0;
+  explicit HostScope(const char* n);
+  ~HostScope();
+};
+
 }  // namespace tcbc

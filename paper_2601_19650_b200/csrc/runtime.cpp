@@ -1,5 +1,7 @@
+#include <chrono>
 // Host runtime: arenas, staging ring, context helpers, TTN handle construction.
 #include "runtime.h"
+#include "prof.h"
 
 #include <algorithm>
 #include <cstring>
@@ -155,7 +157,11 @@ void free_ttn(ttn_s* t) {
 }  // namespace tcbc
 
 void ttn_ctx_s::sync() {
+  const auto t0 = std::chrono::steady_clock::now();
   TTN_CUDA(cudaStreamSynchronize(stream));
+  const double w = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  sync_wait_s += w;
+  tcbc::host_prof_wait(w);
   if (stager) stager->epoch();
   ++host_syncs;
 }

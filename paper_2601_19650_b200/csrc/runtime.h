@@ -73,6 +73,7 @@ struct ttn_ctx_s {
   char* dbuf = nullptr;    // device mirror of small results
   size_t dbuf_size = 0;
   int host_syncs = 0;
+  double sync_wait_s = 0.0;     // host time blocked in sync() (TTN_HOST_PROF diagnostics)
   tcbc::Comm* comm = nullptr;   // multi-GPU apply (ttn_ctx_set_comm)
   std::vector<ttn_ctx_s*> workers;   // concurrent sub-batches (ttn_ctx_set_workers); own streams
   bool owns_stream = false;
