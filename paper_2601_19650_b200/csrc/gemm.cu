@@ -25,6 +25,7 @@
 #include "prof.h"
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 namespace tcbc {
@@ -520,14 +521,12 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
   // tiles get their k range split (deterministic: partials reduced in a second kernel).  All
   // groups go to the device in one staging copy and are timed as one zgemm launch set.
   constexpr int NV = kNumShapes * 4;
-  thread_local std::vector<GemmProblem> all;
-  thread_local std::vector<int> grp;
-  all.clear();
-  grp.clear();
+  thread_local std::vector<unsigned char> grp;
+  grp.assign(n, 255);
   int cnt[NV] = {0};
-  int nsplit = 0;
+  int nsplit = 0, total = 0;
   for (int i = 0; i < n; ++i) {
-    GemmProblem p = h[i];
+    GemmProblem& p = h[i];
     if (p.M <= 0 || p.N <= 0) continue;
     if (p.sym && !(p.M == p.N && p.alpha.y == 0.0 && p.beta.x == 0.0 && p.beta.y == 0.0)) p.sym = 0;
     // A: k-major smem when the innermost m leg is unit-stride and the innermost k leg is not
@@ -564,30 +563,31 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
     }
     const int g = best * 4 + v;
     ++cnt[g];
-    grp.push_back(g);
-    all.push_back(p);
+    grp[i] = (unsigned char)g;
+    ++total;
   }
-  if (all.empty()) return;
-  // order by group (stable), then the split-k problems again for the reduction kernel
+  if (total == 0) return;
+  // grouped order straight into the staging buffer, then the split-k problems again for the
+  // reduction kernel
   int off[NV + 1];
   off[0] = 0;
   for (int g = 0; g < NV; ++g) off[g + 1] = off[g] + cnt[g];
-  const int total = (int)all.size();
-  thread_local std::vector<GemmProblem> ord;
-  ord.resize((size_t)total + nsplit);
+  const size_t stage_bytes = sizeof(GemmProblem) * ((size_t)total + nsplit);
+  GemmProblem* ord = static_cast<GemmProblem*>(st.reserve(stage_bytes));
   {
     int pos[NV];
     for (int g = 0; g < NV; ++g) pos[g] = off[g];
     int sp = total;
-    for (int i = 0; i < total; ++i) {
-      ord[pos[grp[i]]++] = all[i];
-      if (all[i].ksplit > 1) ord[sp++] = all[i];
+    for (int i = 0; i < n; ++i) {
+      if (grp[i] == 255) continue;
+      std::memcpy(&ord[pos[grp[i]]++], &h[i], sizeof(GemmProblem));
+      if (h[i].ksplit > 1) std::memcpy(&ord[sp++], &h[i], sizeof(GemmProblem));
     }
   }
   double flops = 0.0, bytes = 0.0;
   int tiles[NV];
   for (int g = 0; g < NV; ++g) {
-    GemmProblem* q = ord.data() + off[g];
+    GemmProblem* q = ord + off[g];
     switch (g / 4) {
       case 0: tiles[g] = assign_tiles<64, 64>(q, cnt[g], flops, bytes); break;
       case 1: tiles[g] = assign_tiles<128, 32>(q, cnt[g], flops, bytes); break;
@@ -596,7 +596,7 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
       default: tiles[g] = assign_tiles<16, 128>(q, cnt[g], flops, bytes); break;
     }
   }
-  const GemmProblem* d = static_cast<const GemmProblem*>(st.put(ord.data(), sizeof(GemmProblem) * ord.size()));
+  const GemmProblem* d = static_cast<const GemmProblem*>(st.commit(ord, stage_bytes));
 #define TCBC_LV(G, BM, BN, WM, WN)                                                             \
   launch_variant<BM, BN, WM, WN, false, false>(d + off[G + 0], cnt[G + 0], tiles[G + 0], s); \
   launch_variant<BM, BN, WM, WN, false, true>(d + off[G + 1], cnt[G + 1], tiles[G + 1], s);  \

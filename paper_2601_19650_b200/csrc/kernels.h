@@ -2,6 +2,7 @@
 // Every launcher takes a host copy of the problem array (for scheduling) and a device copy
 // (what the kernel reads); both describe the same problems.
 #pragma once
+#include <vector>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -123,7 +124,17 @@ struct ScaleRowsProblem {
 // device pointer stays valid until the owner's next host synchronisation.
 struct Stager {
   virtual void* put(const void* host, size_t bytes) = 0;
+  // Two-phase staging without an intermediate host copy: reserve() returns a host buffer of
+  // `bytes` to fill, commit() enqueues its copy and returns the device pointer.  The default
+  // goes through put().
+  virtual void* reserve(size_t bytes) {
+    tmp_.resize(bytes);
+    return tmp_.data();
+  }
+  virtual void* commit(void* host, size_t bytes) { return put(host, bytes); }
   virtual ~Stager() {}
+ private:
+  std::vector<char> tmp_;
 };
 
 // Launchers fill the scheduling fields of the host problems, stage them, and launch.

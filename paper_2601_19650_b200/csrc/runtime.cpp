@@ -75,6 +75,25 @@ void* RingStager::put(const void* host, size_t bytes) {
   return d;
 }
 
+void* RingStager::reserve(size_t bytes) {
+  size_t b = (bytes + 255) & ~size_t(255);
+  if (b > size_) throw Error(TTN_ERR_UNSUPPORTED, "descriptor array larger than the staging ring");
+  if (off_ + b > size_) {  // wrap: earlier copies must have completed before reuse
+    TTN_CUDA(cudaStreamSynchronize(s_));
+    off_ = 0;
+  }
+  return h_ + off_;
+}
+
+void* RingStager::commit(void* host, size_t bytes) {
+  char* h = static_cast<char*>(host);
+  if (h != h_ + off_) return put(host, bytes);   // not the reserved slot
+  TTN_CUDA(cudaMemcpyAsync(d_ + off_, h, bytes, cudaMemcpyHostToDevice, s_));
+  void* d = d_ + off_;
+  off_ += (bytes + 255) & ~size_t(255);
+  return d;
+}
+
 void RingStager::epoch() { off_ = 0; }
 
 void build_topology(ttn_s* t, const int32_t* parent, int n) {

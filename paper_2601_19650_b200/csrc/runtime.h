@@ -50,6 +50,8 @@ class RingStager : public Stager {
   RingStager(cudaStream_t s, size_t bytes = 64ull << 20);
   ~RingStager();
   void* put(const void* host, size_t bytes) override;
+  void* reserve(size_t bytes) override;
+  void* commit(void* host, size_t bytes) override;
   void epoch();   // call after a stream synchronisation: the whole ring is free again
  private:
   cudaStream_t s_;
