@@ -9,7 +9,7 @@
 //  K1 tridiag  one CTA per matrix: Householder reduction Q^H A Q = T (real symmetric
 //              tridiagonal; the complex reflector makes every off-diagonal real).  n <= 256:
 //              lower triangle only, rank-2 update of step j-1 fused into the Hermitian mat-vec
-//              of step j (one pass per step), the packed triangle in shared memory for n <= 144.
+//              of step j (one pass per step), its trailing rows in shared memory for n <= 144.
 //  K2 bisect   G lanes per (matrix, eigenvalue): Sturm-count multisection for the top kmax
 //              eigenvalues (G sized to the level).
 //  K3 invit    one thread per (matrix, eigenvector): inverse iteration on T - lam I
@@ -108,13 +108,14 @@ constexpr int SMEM_MAX_N = 144;    // matrix (packed lower triangle) resident in
 // Shared-memory budget of the fused path: the fixed vectors, then as many trailing rows of the
 // packed lower triangle as fit (rows >= r0 live in shared memory, rows < r0 stay in global /
 // L2).  The trailing rows are touched by every step, the leading ones only by the first r0
-// steps, so keeping the tail on chip removes most of the L2 traffic (n = 192: r0 ~ 118, the
-// global part is (118/192)^3 ~ 23% of a full-L2 reduction).
-constexpr size_t FUSED_SMEM_BUDGET = 220u << 10;
+// steps, so the on-chip tail carries most of the traffic.  The budget keeps two CTAs per SM
+// (the register limit): measured on config 3's 1024 Grams of order 128, a half-resident
+// triangle with two CTAs per SM beats the fully resident one with one CTA per SM (heev
+// 28 -> 26 ms per step).
+constexpr size_t FUSED_SMEM_BUDGET = 110u << 10;
 __host__ __device__ inline size_t fused_base_bytes(int n) { return (size_t)n * 16 * 2 + (size_t)16 * (3 + 8) * n + 64; }
 // Measured (config 3, n = 192): the reduction is latency-bound (fixed-latency FP64 chains,
-// barriers), not L2-bound, and a partial shared-memory tail costs the second resident CTA per
-// SM; so only matrices that fit entirely (n <= SMEM_MAX_N) go on chip.
+// barriers), not L2-bound; a tail of a few rows buys little there, so n > 144 stays in L2.
 __host__ __device__ inline int fused_r0(int n) {
   if (n > 144) return n;
   const size_t avail = (FUSED_SMEM_BUDGET - fused_base_bytes(n)) / 16;   // complex entries
