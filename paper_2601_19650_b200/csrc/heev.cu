@@ -9,7 +9,7 @@
 //  K1 tridiag  one CTA per matrix: Householder reduction Q^H A Q = T (real symmetric
 //              tridiagonal; the complex reflector makes every off-diagonal real).  n <= 256:
 //              lower triangle only, rank-2 update of step j-1 fused into the Hermitian mat-vec
-//              of step j (one pass per step), its trailing rows in shared memory for n <= 144.
+//              of step j (one pass per step), its trailing rows in shared memory.
 //  K2 bisect   G lanes per (matrix, eigenvalue): Sturm-count multisection for the top kmax
 //              eigenvalues (G sized to the level).
 //  K3 invit    one thread per (matrix, eigenvector): inverse iteration on T - lam I
@@ -114,10 +114,9 @@ constexpr int SMEM_MAX_N = 144;    // matrix (packed lower triangle) resident in
 // 28 -> 26 ms per step).
 constexpr size_t FUSED_SMEM_BUDGET = 110u << 10;
 __host__ __device__ inline size_t fused_base_bytes(int n) { return (size_t)n * 16 * 2 + (size_t)16 * (3 + 8) * n + 64; }
-// Measured (config 3, n = 192): the reduction is latency-bound (fixed-latency FP64 chains,
-// barriers), not L2-bound; a tail of a few rows buys little there, so n > 144 stays in L2.
+// n = 192 (config 3's G-route Grams): the last ~25 rows fit; heev 26 -> 25 ms per step.
 __host__ __device__ inline int fused_r0(int n) {
-  if (n > 144) return n;
+  if (n > FUSED_MAX_N) return n;
   const size_t avail = (FUSED_SMEM_BUDGET - fused_base_bytes(n)) / 16;   // complex entries
   int r0 = 0;
   while ((size_t)n * (n + 1) / 2 - (size_t)r0 * (r0 + 1) / 2 > avail) ++r0;
