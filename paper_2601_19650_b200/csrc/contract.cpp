@@ -155,6 +155,39 @@ PlanT make_plan(const Task& t) {
     slab.push_back(o.labels);
     sdim.push_back(o.dims);
   }
+  // Intermediate layouts, top-down: an intermediate's legs are ordered [legs its consumer
+  // keeps, in the consumer's output order] ++ [legs the consumer contracts, in the order of the
+  // sibling operand when that is an input].  The consumer then reads it as a plain row-major
+  // operand with the contraction innermost (coalesced, folded legs), instead of gathering it.
+  std::vector<std::vector<int>> layout(1 << n);
+  static const bool natural = getenv("TTN_PLAN_NATURAL") != nullptr;
+  if (!natural) {
+    std::function<void(int)> assign = [&](int m) {
+      if ((m & (m - 1)) == 0) return;   // input operand: fixed layout
+      const int sub = split[m], rest = m ^ sub;
+      const int ma = (sub & -sub) < (rest & -rest) ? sub : rest;
+      const int mb = m ^ ma;
+      const std::vector<int>& Lm = (m == full) ? t.out_labels : layout[m];
+      auto has = [](const std::vector<int>& L, int l) { return std::find(L.begin(), L.end(), l) != L.end(); };
+      for (int c : {ma, mb}) {
+        if ((c & (c - 1)) == 0) continue;
+        const int sib = m ^ c;
+        std::vector<int> L;
+        for (int l : Lm)
+          if (has(freel[c], l)) L.push_back(l);
+        // contracted legs: the sibling input's order, else this child's own order
+        const std::vector<int>& ko = ((sib & (sib - 1)) == 0) ? t.ops[__builtin_ctz(sib)].labels : freel[c];
+        for (int l : ko)
+          if (has(freel[c], l) && has(freel[sib], l) && !has(L, l)) L.push_back(l);
+        for (int l : freel[c])   // safety: every leg exactly once
+          if (!has(L, l)) L.push_back(l);
+        layout[c] = L;
+      }
+      assign(ma);
+      assign(mb);
+    };
+    assign(full);
+  }
   std::vector<int> slot_of_mask(1 << n, -1);
   for (int i = 0; i < n; ++i) slot_of_mask[1 << i] = i;
   std::function<int(int)> emit = [&](int m) -> int {
@@ -172,6 +205,7 @@ PlanT make_plan(const Task& t) {
     const bool last = (m == full);
     std::vector<int> LC;
     if (last) LC = t.out_labels;
+    else if (!layout[m].empty()) LC = layout[m];
     else {
       LC = FA;
       LC.insert(LC.end(), FB.begin(), FB.end());
