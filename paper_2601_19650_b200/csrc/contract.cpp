@@ -175,8 +175,9 @@ PlanT make_plan(const Task& t) {
         std::vector<int> L;
         for (int l : Lm)
           if (has(freel[c], l)) L.push_back(l);
-        // contracted legs: the sibling input's order, else this child's own order
-        const std::vector<int>& ko = ((sib & (sib - 1)) == 0) ? t.ops[__builtin_ctz(sib)].labels : freel[c];
+        // contracted legs: the sibling input's order; between two intermediates one common
+        // order (the A side's), so the consumer's k legs fold in both operands
+        const std::vector<int>& ko = ((sib & (sib - 1)) == 0) ? t.ops[__builtin_ctz(sib)].labels : freel[ma];
         for (int l : ko)
           if (has(freel[c], l) && has(freel[sib], l) && !has(L, l)) L.push_back(l);
         for (int l : freel[c])   // safety: every leg exactly once
@@ -313,6 +314,15 @@ void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st) 
     for (auto& g : probs) {
       std::ostringstream o;
       o << g.M << "x" << g.N << "x" << g.K << " legs" << g.nm << g.nn << g.nk << " c" << g.conjA << g.conjB;
+      if ((double)g.M * g.N * g.K > 5e7) {
+        o << " [m";
+        for (int q = 0; q < g.nm; ++q) o << " " << g.md[q] << ":" << g.am[q] << "/" << g.cm[q];
+        o << " n";
+        for (int q = 0; q < g.nn; ++q) o << " " << g.nd[q] << ":" << g.bn[q] << "/" << g.cn[q];
+        o << " k";
+        for (int q = 0; q < g.nk; ++q) o << " " << g.kd[q] << ":" << g.ak[q] << "/" << g.bk[q];
+        o << "]";
+      }
       shapes[o.str()] += 1;
     }
     fprintf(stderr, "[gemm] %zu problems:", probs.size());
