@@ -128,6 +128,8 @@ __host__ __device__ inline int fused_r0(int n) {
 // pass over the trailing triangle per step.  Rows >= r0 of the packed triangle live in shared
 // memory (r0 = 0: all of it), rows < r0 in the global A.
 // Reflector j is written to row j (columns > j) of the global A for the back-transform.
+// NQ: 32-column blocks per row (n <= 32 NQ).
+template <int NQ>
 __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, cplx* vcur, cplx* wcur, cplx* base,
                               double* dvec, double* evec, cplx* tau_out, double2* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -197,31 +199,41 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
       tau_out[j] = tau;
     }
     __syncthreads();
-    // (c) one pass over the trailing lower triangle: apply U_{j-1}, accumulate p = A v_j
-    cplx cacc[8];
+    // (c) one pass over the trailing lower triangle: apply U_{j-1}, accumulate p = A v_j.
+    // All of a row's entries are loaded before any is used (one memory round trip per row,
+    // not one per 32-column block).
+    cplx cacc[NQ];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) cacc[q] = make_double2(0.0, 0.0);
+    for (int q = 0; q < NQ; ++q) cacc[q] = make_double2(0.0, 0.0);
     for (int r = j + 1 + warp; r < n; r += HEEV_WARPS) {
+      const int nq = (r - j + 31) >> 5;   // column blocks that reach the diagonal (warp-uniform)
+      cplx a[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int c = j + 1 + lane + 32 * q;
+        a[q] = (q < nq && c <= r) ? LL(r, c) : make_double2(0.0, 0.0);
+      }
       const cplx vr = vcur[r];
       const cplx vpr = vprev[r], wpr = wprev[r];
       double sr = 0.0, si = 0.0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NQ; ++q) {
+        if (q >= nq) break;
         const int c = j + 1 + lane + 32 * q;
-        if (c > r) break;
-        cplx a = LL(r, c);
+        if (c > r) continue;
+        cplx av = a[q];
         if (have_prev) {
           const cplx vpc = vprev[c], wpc = wprev[c];
-          a.x -= (vpr.x * wpc.x + vpr.y * wpc.y) + (wpr.x * vpc.x + wpr.y * vpc.y);
-          a.y -= (vpr.y * wpc.x - vpr.x * wpc.y) + (wpr.y * vpc.x - wpr.x * vpc.y);
-          LL(r, c) = a;
+          av.x -= (vpr.x * wpc.x + vpr.y * wpc.y) + (wpr.x * vpc.x + wpr.y * vpc.y);
+          av.y -= (vpr.y * wpc.x - vpr.x * wpc.y) + (wpr.y * vpc.x - wpr.x * vpc.y);
+          LL(r, c) = av;
         }
         const cplx vc = vcur[c];
-        sr += a.x * vc.x - a.y * vc.y;
-        si += a.x * vc.y + a.y * vc.x;
+        sr += av.x * vc.x - av.y * vc.y;
+        si += av.x * vc.y + av.y * vc.x;
         if (c < r) {   // (r, c) also stands for A[c][r] = conj(a): p[c] += conj(a) v_r
-          cacc[q].x += a.x * vr.x + a.y * vr.y;
-          cacc[q].y += a.x * vr.y - a.y * vr.x;
+          cacc[q].x += av.x * vr.x + av.y * vr.y;
+          cacc[q].y += av.x * vr.y - av.y * vr.x;
         }
       }
       sr = warp_sum(sr);
@@ -229,7 +241,7 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
       if (lane == 0) prow[r] = make_double2(sr, si);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int c = j + 1 + lane + 32 * q;
       if (c < n) colpart[warp * n + c] = cacc[q];
     }
@@ -404,6 +416,7 @@ __device__ void tridiag_stats(const HeevProblem& P, double trace) {
 }
 
 // ---------------------------------------------------------------- K1: tridiagonalisation
+template <int NQ>
 __global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
   const int n = P.n;
@@ -419,7 +432,7 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* 
   double tr = 0.0;
   for (int i = tid; i < n; i += HEEV_THREADS) tr += A[(size_t)i * n + i].x;
   const double trace = block_sum2(tr, 0.0, red).x;
-  if (n <= FUSED_MAX_N) tridiag_fused(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
+  if (n <= 32 * NQ) tridiag_fused<NQ>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
   else tridiag_full(A, n, sv, sp, dvec, evec, P.tau, red);
   tridiag_stats(P, trace);
 }
@@ -1415,7 +1428,9 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(heev_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
+    cudaFuncSetAttribute(heev_tridiag<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
+    cudaFuncSetAttribute(heev_tridiag<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
+    cudaFuncSetAttribute(heev_tridiag<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
     attr = true;
   }
   int total = 0;
@@ -1462,7 +1477,11 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
     size_t smem = 0;
     for (auto& p : g) smem = std::max(smem, heev_smem_bytes(p.n, p.kmax));
     const HeevProblem* dg = static_cast<const HeevProblem*>(st.put(g.data(), sizeof(HeevProblem) * g.size()));
-    heev_tridiag<<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
+    int mxn = 0;
+    for (auto& p : g) mxn = std::max(mxn, p.n);
+    if (mxn <= 128) heev_tridiag<4><<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
+    else if (mxn <= 192) heev_tridiag<6><<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
+    else heev_tridiag<8><<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
     count_launch();
   }
   {   // smallest lanes-per-eigenvalue that still keeps ~12 warps per SM busy
