@@ -357,7 +357,7 @@ def run_native(args, rank, world, local_rank):
         dist.barrier()
     launches = P.ttn_launch_count() - lc0
     prof = {fam: P.ttn_profile_read(fam) for fam in ("all", "zgemm", "heev", "heev_large", "potrf", "trtri", "geqr", "permute",
-                                                     "scale_rows", "misc")}
+                                                     "scale_rows", "misc", "gap_after_sync")}
     P.ttn_profile_enable(False)
     clk = clocks.stop(local_rank) if clocks else None
 
@@ -455,17 +455,22 @@ def run_native(args, rank, world, local_rank):
         showcase = config4_showcase(ctx, stream)
     g = prof["zgemm"]
     ach = g["flops"] / (g["ms"] / 1000.0) / 1e12 if g["ms"] > 0 else 0.0
+    # DRAM traffic of the zgemm launches of one step of this config (committed ncu capture),
+    # per profiler launch (one launch_gemm call: its variant kernels back to back) like `achieved`
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_zgemm_traffic_r01.json")
-    if os.path.exists(tp):
+    tp = os.path.join(ROOT, "profiles", f"ncu_zgemm_traffic_r01_c{cfg}.json")
+    if os.path.exists(tp) and g["launches"]:
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
+            traffic = json.load(open(tp))["bytes_per_step"] / (g["launches"] / args.steps)
         except Exception:
             traffic = None
     value = applies_all / (ms_max / 1000.0)
+    gap = prof.pop("gap_after_sync")
     kern = {k: {"ms": v["ms"], "share_of_kernel_time": v["ms"] / prof["all"]["ms"] if prof["all"]["ms"] else None,
                 "launches": v["launches"], "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 else None}
             for k, v in prof.items() if v["launches"]}
+    # device idle between a host synchronisation (data-dependent ranks) and the next launch set
+    kern["idle_after_sync"] = {"ms": gap["ms"], "syncs": gap["launches"]}
     line = {
         "metric": "CBC TTNO.TTNS applies/sec (FP64)",
         "value": value,
@@ -490,8 +495,8 @@ def run_native(args, rank, world, local_rank):
                      "flops_per_launch": g["flops"] / max(g["launches"], 1),
                      "algorithmic_bytes_per_launch": g["bytes"] / max(g["launches"], 1),
                      "ms_per_launch": g["ms"] / max(g["launches"], 1),
-                     "traffic_source": "profiles/ncu_zgemm_traffic_r01.json: mean DRAM read+write over every zgemm "
-                                       "launch of one config-3 step (ncu, cold-cache replays)"},
+                     "traffic_source": f"profiles/ncu_zgemm_traffic_r01_c{cfg}.json: DRAM read+write of every "
+                                       "zgemm_grouped kernel of one step (ncu, cold-cache replays) / launch sets per step"},
         "kernels": kern,
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -90,6 +90,7 @@ ttn_status ttn_ctx_destroy(ttn_ctx ctx) {
   delete ctx->stager;
   delete ctx->comm;
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
+  if (ctx->rank_ev) cudaEventDestroy(ctx->rank_ev);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TTN_OK;

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <map>
 
 namespace tcbc {
@@ -174,6 +175,18 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       cudaMemcpy(gcopy.back().data(), h.A, sizeof(cplx) * h.n * h.n, cudaMemcpyDeviceToHost);
     }
   }
+  static const bool dbg = getenv("TTN_DEBUG_HEEV") != nullptr;
+  // ranks and discarded weights go to the host as soon as the eigenvalue stages have fixed them:
+  // the host waits on that point only, and builds the next level while the eigenvector stages
+  // and the factor kernels still run (the next level's launches queue behind them)
+  ctx->ensure_small(sizeof(int) * nj + sizeof(double) * nj);
+  int* hk = reinterpret_cast<int*>(ctx->hbuf);
+  double* hw = reinterpret_cast<double*>(ctx->hbuf + sizeof(int) * ((nj + 1) & ~1));
+  auto read_ranks = [&]() {
+    TTN_CUDA(cudaMemcpyAsync(hk, d_k, sizeof(int) * nj, cudaMemcpyDeviceToHost, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(hw, d_w, sizeof(double) * nj, cudaMemcpyDeviceToHost, ctx->stream));
+  };
+  bool early = false;
   {   // small Grams: tridiagonal pipeline (heev.cu); large ones: Chebyshev subspace (chfsi.cu)
     std::vector<HeevProblem> small;
     std::vector<HeevProblem*> large;
@@ -181,19 +194,24 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       if (chfsi_applicable(h.n, h.kmax)) large.push_back(&h);
       else small.push_back(h);
     }
-    if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream);
+    std::function<void()> ready;
+    if (large.empty() && !dbg)
+      ready = [&]() {
+        read_ranks();
+        ctx->mark_ranks();
+        early = true;
+      };
+    if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream, ready);
     chfsi_heev(ctx, large, st);
   }
   if (!sr.empty()) launch_scale_rows(sr.data(), (int)sr.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, fgemm, st);
-  // read ranks and discarded weights
-  ctx->ensure_small(sizeof(int) * nj + sizeof(double) * nj);
-  int* hk = reinterpret_cast<int*>(ctx->hbuf);
-  double* hw = reinterpret_cast<double*>(ctx->hbuf + sizeof(int) * ((nj + 1) & ~1));
-  TTN_CUDA(cudaMemcpyAsync(hk, d_k, sizeof(int) * nj, cudaMemcpyDeviceToHost, ctx->stream));
-  TTN_CUDA(cudaMemcpyAsync(hw, d_w, sizeof(double) * nj, cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->sync();
-  static const bool dbg = getenv("TTN_DEBUG_HEEV") != nullptr;
+  if (early) {
+    ctx->wait_ranks();
+  } else {
+    read_ranks();
+    ctx->sync();
+  }
   if (dbg) {   // debug: every eigenvector block and factor must be finite
     for (int j = 0; j < nj; ++j) {
       const HeevProblem& h = hp[j];

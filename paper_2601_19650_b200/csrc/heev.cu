@@ -1107,15 +1107,18 @@ __global__ void heev_backtr(const HeevProblem* __restrict__ probs, int nprob, in
 }
 
 // K7: eigenvalues and discarded weight back to the unscaled data (HeevProblem::exp2)
-__global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob) {
+// what: 1 = the discarded weight (right after K6, so the host can read k and w early),
+// 2 = the eigenvalues (after inverse iteration, which shifts by the scaled values)
+__global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob, int what) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nprob) return;
   const HeevProblem& P = probs[i];
   if (!P.exp2) return;
   const int e = pow2_effective(*P.exp2);
   if (e == 0) return;
-  for (int t = 0; t < P.kmax; ++t) P.lam[t] = ldexp(P.lam[t], 2 * e);
-  if (P.w_out) *P.w_out = ldexp(*P.w_out, 2 * e);
+  if (what & 2)
+    for (int t = 0; t < P.kmax; ++t) P.lam[t] = ldexp(P.lam[t], 2 * e);
+  if ((what & 1) && P.w_out) *P.w_out = ldexp(*P.w_out, 2 * e);
 }
 
 // K5 for n <= 32 * NQ, one CTA per (matrix, 8 eigenvectors): the eigenvector lives in its
@@ -1423,7 +1426,7 @@ void launch_tridiag_cluster(const HeevProblem* d, int nprob, int cs, size_t smem
 }
 }  // namespace
 
-void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
+void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::function<void()>& values_ready) {
   HostScope hs_("launch_heev");
   if (n == 0) return;
   static bool attr = false;
@@ -1498,6 +1501,8 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
     }
   }
   heev_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);   // k and w: only kept pairs go on
+  heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n, 1);
+  if (values_ready) values_ready();   // k and w are final: the caller may read them now
   {
     int mxn = 1;
     for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
@@ -1547,7 +1552,8 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s) {
       heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
     }
   }
-  heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n);
+  heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n, 2);
+  count_launch();
   count_launch();
   count_launch(); count_launch(); count_launch(); count_launch(); count_launch();
   prof_end(s, "heev", fl, by);

@@ -2,6 +2,7 @@
 // Every launcher takes a host copy of the problem array (for scheduling) and a device copy
 // (what the kernel reads); both describe the same problems.
 #pragma once
+#include <functional>
 #include <vector>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -140,7 +141,11 @@ struct Stager {
 // Launchers fill the scheduling fields of the host problems, stage them, and launch.
 void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws = nullptr);
 void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s);
-void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s);
+// values_ready (optional) is called once the ranks (k_out) and discarded weights (w_out) are
+// final in stream order -- before the eigenvector stages are enqueued -- so a caller can start
+// reading them while the vectors are still being computed.
+void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s,
+                 const std::function<void()>& values_ready = std::function<void()>());
 void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_scale_rows(ScaleRowsProblem* h, int n, Stager& st, cudaStream_t s);

@@ -50,6 +50,11 @@ struct Profiler {
       a.flops += p.flops;
       a.bytes += p.bytes;
       a.launches += 1;
+      if (p.family == "gap_after_sync") {   // idle time, not kernel time
+        pool.push_back(p.a);
+        pool.push_back(p.b);
+        continue;
+      }
       Acc& t = acc["all"];
       t.ms += ms;
       t.flops += p.flops;
@@ -68,13 +73,29 @@ Profiler& P() {
 }
 
 thread_local cudaEvent_t t_open = nullptr;   // per host thread (worker contexts run concurrently)
+thread_local cudaEvent_t t_gap = nullptr;    // recorded right after a host synchronisation
 
 }  // namespace
+
+void prof_mark_sync(cudaStream_t s) {
+  Profiler& p = P();
+  if (!p.on) return;
+  std::lock_guard<std::mutex> g(p.mu);
+  if (t_gap) p.pool.push_back(t_gap);
+  t_gap = p.get();
+  cudaEventRecord(t_gap, s);
+}
 
 void prof_begin(cudaStream_t s) {
   Profiler& p = P();
   if (!p.on) return;
   std::lock_guard<std::mutex> g(p.mu);
+  if (t_gap) {   // device idle from the synchronisation to this launch set: host work in between
+    cudaEvent_t e = p.get();
+    cudaEventRecord(e, s);
+    p.pending.push_back(Pending{t_gap, e, "gap_after_sync", 0.0, 0.0});
+    t_gap = nullptr;
+  }
   t_open = p.get();
   cudaEventRecord(t_open, s);
 }

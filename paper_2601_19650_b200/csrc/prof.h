@@ -7,6 +7,7 @@
 namespace tcbc {
 
 void prof_begin(cudaStream_t s);                       // no-op unless enabled
+void prof_mark_sync(cudaStream_t s);                   // after a host synchronisation of s
 void prof_end(cudaStream_t s, const char* family, double flops, double bytes);
 void prof_enable(bool on);
 bool prof_read(const char* family, double* ms, double* flops, double* bytes, long long* launches);

@@ -181,7 +181,22 @@ void ttn_ctx_s::sync() {
   const double w = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   sync_wait_s += w;
   tcbc::host_prof_wait(w);
+  tcbc::prof_mark_sync(stream);
   if (stager) stager->epoch();
+  ++host_syncs;
+}
+
+void ttn_ctx_s::mark_ranks() {
+  if (!rank_ev) TTN_CUDA(cudaEventCreateWithFlags(&rank_ev, cudaEventDisableTiming));
+  TTN_CUDA(cudaEventRecord(rank_ev, stream));
+}
+
+void ttn_ctx_s::wait_ranks() {
+  const auto t0 = std::chrono::steady_clock::now();
+  TTN_CUDA(cudaEventSynchronize(rank_ev));
+  const double w = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  sync_wait_s += w;
+  tcbc::host_prof_wait(w);
   ++host_syncs;
 }
 

@@ -81,6 +81,11 @@ struct ttn_ctx_s {
   bool owns_stream = false;
   int parts = 1;                // subtree groups of a partitioned apply
   void sync();             // cudaStreamSynchronize + stager epoch
+  // partial synchronisation: mark a point in the stream, then wait for it only (the work
+  // enqueued after the mark keeps running; the staging ring is not recycled)
+  cudaEvent_t rank_ev = nullptr;
+  void mark_ranks();
+  void wait_ranks();
   void ensure_small(size_t bytes);
 };
 

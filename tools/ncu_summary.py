@@ -76,8 +76,8 @@ def full(src, dst, traffic=None):
         json.dump({"bytes_per_launch": sum(tb) / len(tb), "launches": len(tb), "source": src}, open(traffic, "w"), indent=1)
 
 
-def traffic(src, dst_md, dst_json):
-    """Per-launch DRAM bytes of every zgemm launch of one step (ncu --metrics CSV)."""
+def traffic(src, dst_md, dst_json, applies=2):
+    """DRAM bytes of every zgemm launch in an ncu --metrics CSV of `applies` bench steps."""
     rows = [r for r in csv.reader(open(src)) if len(r) > 10]
     h = rows[0]
     ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
@@ -91,10 +91,10 @@ def traffic(src, dst_md, dst_json):
             continue
         per[r[idk]][r[mi]] = v
         per[r[idk]]["name"] = r[ki].split("(")[0]
-    launches = [d for d in per.values() if "dram__bytes_read.sum" in d]
+    launches = [d for d in per.values() if "dram__bytes_read.sum" in d and "zgemm_grouped" in d["name"]]
     tot_b = sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in launches)
     tot_t = sum(d.get("gpu__time_duration.sum", 0.0) for d in launches)
-    out = [f"# zgemm DRAM traffic per launch, one config-3 step ({src})", "",
+    out = [f"# zgemm DRAM traffic per launch ({src}, {applies} bench steps)", "",
            f"launches: {len(launches)}; mean DRAM bytes per launch: {tot_b / len(launches) / 1e6:.1f} MB; "
            f"mean achieved DRAM bandwidth {tot_b / tot_t / 1e9:.0f} GB/s (cold-cache, serialised replays)", "",
            "| launch | kernel | time us | DRAM read MB | DRAM write MB | DMMA active % |", "|---:|---|---:|---:|---:|---:|"]
@@ -103,15 +103,17 @@ def traffic(src, dst_md, dst_json):
                    f"{d['dram__bytes_read.sum'] / 1e6:.1f} | {d['dram__bytes_write.sum'] / 1e6:.1f} | "
                    f"{d.get('sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active', 0):.1f} |")
     open(dst_md, "w").write("\n".join(out) + "\n")
-    json.dump({"bytes_per_launch": tot_b / len(launches), "launches": len(launches), "source": src,
-               "note": "mean over every zgemm launch of one bench step (ncu --metrics dram__bytes_read/write.sum)"},
+    json.dump({"bytes_per_step": tot_b / applies, "kernel_launches_per_step": len(launches) / applies,
+               "bytes_per_kernel_launch": tot_b / len(launches), "source": src,
+               "note": "DRAM read+write of every zgemm_grouped launch of one bench step (ncu --metrics "
+                       "dram__bytes_read/write.sum, cold-cache serialised replays)"},
               open(dst_json, "w"), indent=1)
     print("\n".join(out[:4]))
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "traffic":
-        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4], int(sys.argv[5]) if len(sys.argv) > 5 else 2)
         sys.exit(0)
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
