@@ -66,6 +66,24 @@ __device__ double2 block_sum2(double a, double b, double2* red) {
   return r;
 }
 
+// block-wide sum with one barrier: warp partials into buffer `parity` of red[2][HEEV_WARPS],
+// every thread adds them in the same order.  Two calls between barriers must alternate parity.
+__device__ __forceinline__ double2 block_sum2_1b(double a, double b, double2* red, int parity) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* buf = red + parity * HEEV_WARPS;
+  if (lane == 0) buf[warp] = make_double2(a, b);
+  __syncthreads();
+  double2 r = buf[0];
+#pragma unroll
+  for (int w = 1; w < HEEV_WARPS; ++w) {
+    r.x += buf[w].x;
+    r.y += buf[w].y;
+  }
+  return r;
+}
+
 __device__ __forceinline__ unsigned hash32(unsigned x) {
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
   return x;
@@ -148,26 +166,30 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
   }
   __syncthreads();
   bool have_prev = false;
+  cplx a2_prev = make_double2(0.0, 0.0);
   for (int j = 0; j < n - 1; ++j) {
-    // (a) pending update U_{j-1} on column j (rows >= j)
-    if (have_prev) {
-      const cplx vpj = vprev[j], wpj = wprev[j];
+    // (a) pending update U_{j-1} on column j (rows >= j), fused with (b)'s |x|^2 partials:
+    // each thread sums the entries it just updated, so the only barrier is the reduction's
+    double part = 0.0;
+    {
+      // pivot entries of U_{j-1} from data every thread can see (vcur[j] from step j-1's
+      // reflector, wcur[j] from before its reduction barrier), not another thread's vprev / wprev
+      const cplx vpj = vcur[j], wq = wcur[j];
+      const cplx wpj = make_double2(wq.x + a2_prev.x * vpj.x - a2_prev.y * vpj.y,
+                                    wq.y + a2_prev.x * vpj.y + a2_prev.y * vpj.x);
       for (int r = j + tid; r < n; r += HEEV_THREADS) {
         cplx a = LL(r, j);
-        const cplx vr = vprev[r], wr = wprev[r];
-        a.x -= (vr.x * wpj.x + vr.y * wpj.y) + (wr.x * vpj.x + wr.y * vpj.y);
-        a.y -= (vr.y * wpj.x - vr.x * wpj.y) + (wr.y * vpj.x - wr.x * vpj.y);
-        LL(r, j) = a;
+        if (have_prev) {
+          const cplx vr = vprev[r], wr = wprev[r];
+          a.x -= (vr.x * wpj.x + vr.y * wpj.y) + (wr.x * vpj.x + wr.y * vpj.y);
+          a.y -= (vr.y * wpj.x - vr.x * wpj.y) + (wr.y * vpj.x - wr.x * vpj.y);
+          LL(r, j) = a;
+        }
+        if (r >= j + 2) part += a.x * a.x + a.y * a.y;
       }
-      __syncthreads();
     }
     // (b) reflector H_j from x = A[j+1:, j]  (zlarfg)
-    double part = 0.0;
-    for (int r = j + 2 + tid; r < n; r += HEEV_THREADS) {
-      const cplx x = LL(r, j);
-      part += x.x * x.x + x.y * x.y;
-    }
-    const double xn2 = block_sum2(part, 0.0, red).x;
+    const double xn2 = block_sum2_1b(part, 0.0, red, 0).x;
     const cplx alpha = LL(j + 1, j);
     double beta;
     cplx tau, scale;
@@ -207,11 +229,14 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
     for (int q = 0; q < NQ; ++q) cacc[q] = make_double2(0.0, 0.0);
     for (int r = j + 1 + warp; r < n; r += HEEV_WARPS) {
       const int nq = (r - j + 31) >> 5;   // column blocks that reach the diagonal (warp-uniform)
+      // the row's storage (shared-memory tail or global), as one generic pointer: no per-entry
+      // branch; entries past the diagonal are masked by selects, not branches
+      cplx* rowp = r >= r0 ? Ap + ((size_t)r * (r + 1) / 2 - pbase) : A + (size_t)r * n;
       cplx a[NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int c = j + 1 + lane + 32 * q;
-        a[q] = (q < nq && c <= r) ? LL(r, c) : make_double2(0.0, 0.0);
+        a[q] = (q < nq && c <= r) ? rowp[c] : make_double2(0.0, 0.0);
       }
       const cplx vr = vcur[r];
       const cplx vpr = vprev[r], wpr = wprev[r];
@@ -220,21 +245,24 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
       for (int q = 0; q < NQ; ++q) {
         if (q >= nq) break;
         const int c = j + 1 + lane + 32 * q;
-        if (c > r) continue;
+        const bool in = c <= r;
+        const int cc = in ? c : r;   // in-range index for the vector reads
         cplx av = a[q];
         if (have_prev) {
-          const cplx vpc = vprev[c], wpc = wprev[c];
+          const cplx vpc = vprev[cc], wpc = wprev[cc];
           av.x -= (vpr.x * wpc.x + vpr.y * wpc.y) + (wpr.x * vpc.x + wpr.y * vpc.y);
           av.y -= (vpr.y * wpc.x - vpr.x * wpc.y) + (wpr.y * vpc.x - wpr.x * vpc.y);
-          LL(r, c) = av;
+          if (in) rowp[c] = av;
+          av.x = in ? av.x : 0.0;
+          av.y = in ? av.y : 0.0;
         }
-        const cplx vc = vcur[c];
+        const cplx vc = vcur[cc];
         sr += av.x * vc.x - av.y * vc.y;
         si += av.x * vc.y + av.y * vc.x;
-        if (c < r) {   // (r, c) also stands for A[c][r] = conj(a): p[c] += conj(a) v_r
-          cacc[q].x += av.x * vr.x + av.y * vr.y;
-          cacc[q].y += av.x * vr.y - av.y * vr.x;
-        }
+        // (r, c) also stands for A[c][r] = conj(a): p[c] += conj(a) v_r (strictly below the diagonal)
+        const double wx = c < r ? vr.x : 0.0, wy = c < r ? vr.y : 0.0;
+        cacc[q].x += av.x * wx + av.y * wy;
+        cacc[q].y += av.x * wy - av.y * wx;
       }
       sr = warp_sum(sr);
       si = warp_sum(si);
@@ -260,21 +288,19 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
       dr += p.x * v.x + p.y * v.y;
       di += p.x * v.y - p.y * v.x;
     }
-    const double2 dot = block_sum2(dr, di, red);
+    const double2 dot = block_sum2_1b(dr, di, red, 1);
     const cplx a2 = make_double2(-0.5 * (tau.x * dot.x - tau.y * dot.y), -0.5 * (tau.x * dot.y + tau.y * dot.x));
-    for (int r = tid; r < n; r += HEEV_THREADS) {
-      if (r <= j) {
-        vprev[r] = make_double2(0.0, 0.0);
-        wprev[r] = make_double2(0.0, 0.0);
-      } else {
-        const cplx v = vcur[r], p = wcur[r];
-        vprev[r] = v;
-        wprev[r] = make_double2(p.x + a2.x * v.x - a2.y * v.y, p.y + a2.x * v.y + a2.y * v.x);
-      }
+    // same row ownership as the loop above and as the next step's (a): no barrier needed here
+    // (the next step reads other rows' vprev / wprev only after its reduction barriers)
+    for (int r = j + 1 + tid; r < n; r += HEEV_THREADS) {
+      const cplx v = vcur[r], p = wcur[r];
+      vprev[r] = v;
+      wprev[r] = make_double2(p.x + a2.x * v.x - a2.y * v.y, p.y + a2.x * v.y + a2.y * v.x);
     }
+    a2_prev = a2;
     have_prev = tnz;
-    __syncthreads();
   }
+  __syncthreads();
   if (tid == 0) {
     cplx a = LL(n - 1, n - 1);
     if (have_prev) {
@@ -426,7 +452,7 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* 
   cplx* sv = reinterpret_cast<cplx*>(smem_raw);
   cplx* sp = sv + n;
   cplx* base = sp + n;
-  __shared__ double2 red[HEEV_WARPS + 1];
+  __shared__ double2 red[2 * HEEV_WARPS + 1];
   double* dvec = P.work;
   double* evec = P.work + n;
   double tr = 0.0;
