@@ -33,17 +33,23 @@ namespace tcbc {
 namespace {
 
 constexpr int BK = 8, STAGES = 3, THREADS = 128;
+#ifndef TCBC_SKINNY_ST
+#define TCBC_SKINNY_ST 2
+#endif
+#ifndef TCBC_SKINNY_MINB
+#define TCBC_SKINNY_MINB 3
+#endif
 constexpr int PADK = BK + 4;   // m-major / n-major rows: 12 complex = 192 B (conflict-free frags)
 
 // k-major rows (As[k][m], Bs[k][n]) are padded by 2 complex (32 B): the 4 k-rows a fragment
 // load touches then start in different bank quarters (no 4-way conflicts)
-template <int BM, int BN, bool AKM, bool BNM>
+template <int BM, int BN, bool AKM, bool BNM, int ST>
 struct Cfg {
   static constexpr int LDAK = BM + 2, LDBK = BN + 2;
   static constexpr int A_ELEMS = AKM ? BK * LDAK : BM * PADK;
   static constexpr int B_ELEMS = BNM ? BN * PADK : BK * LDBK;
-  static constexpr int TAB = (2 * (3 * BM + 3 * BN) + 2 * STAGES * BK) * 8;
-  static constexpr int BYTES = STAGES * (A_ELEMS + B_ELEMS) * 16 + TAB + 2 * (int)sizeof(GemmProblem) + 64;
+  static constexpr int TAB = (2 * (3 * BM + 3 * BN) + 2 * ST * BK) * 8;
+  static constexpr int BYTES = ST * (A_ELEMS + B_ELEMS) * 16 + TAB + 2 * (int)sizeof(GemmProblem) + 64;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -101,10 +107,10 @@ __device__ __forceinline__ int find_problem(const GemmProblem* p, int n, int til
 // and its first STAGES-1 operand stages are in flight (cp.async) while this tile's epilogue
 // stores its accumulators: the prologue latency of short-K tiles (config 3's K = 32 steps)
 // hides behind the epilogue instead of idling the tensor pipe.
-template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
-__global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob,
+template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM, int ST, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob,
                                                             int total_tiles) {
-  using C_ = Cfg<BM, BN, AKM, BNM>;
+  using C_ = Cfg<BM, BN, AKM, BNM, ST>;
   constexpr int WTM = BM / WGM, WTN = BN / WGN;     // warp tile
   constexpr int TM = WTM / 8, TN = WTN / 8;         // DMMA tiles per warp
   constexpr int TABN = 3 * BM + 3 * BN;             // offsets per table buffer
@@ -114,11 +120,11 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
   static_assert((BM * BK) % THREADS == 0 && (BN * BK) % THREADS == 0, "load mapping");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
-  cplx* Bs = As + STAGES * C_::A_ELEMS;
-  long long* tab = reinterpret_cast<long long*>(Bs + STAGES * C_::B_ELEMS);   // [2][TABN]
-  long long* kA = tab + 2 * TABN;            // [STAGES][BK] k-leg offsets into A (-1: k >= K)
-  long long* kB = kA + STAGES * BK;          // [STAGES][BK] k-leg offsets into B
-  GemmProblem* sP = reinterpret_cast<GemmProblem*>(kB + STAGES * BK);   // [2]
+  cplx* Bs = As + ST * C_::A_ELEMS;
+  long long* tab = reinterpret_cast<long long*>(Bs + ST * C_::B_ELEMS);   // [2][TABN]
+  long long* kA = tab + 2 * TABN;            // [ST][BK] k-leg offsets into A (-1: k >= K)
+  long long* kB = kA + ST * BK;          // [ST][BK] k-leg offsets into B
+  GemmProblem* sP = reinterpret_cast<GemmProblem*>(kB + ST * BK);   // [2]
   int* sPi = reinterpret_cast<int*>(sP + 2);                            // [2] problem index
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -183,19 +189,19 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
       if (T.mirror) rowCn[i] = n < P.N ? goff(n, P.nm, P.md, P.cm) : -1;
     }
     if (P.nk != 1)
-      for (int j = tid; j < 2 * BK * STAGES; j += THREADS) {
+      for (int j = tid; j < 2 * BK * ST; j += THREADS) {
         const int Tk = j / (2 * BK), jj = j % (2 * BK);
         if (Tk < T.ktiles) {
           const int kl = jj % BK, k = T.kbeg + Tk * BK + kl;
-          if (jj < BK) kA[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.ak) : -1;
-          else kB[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.bk) : -1;
+          if (jj < BK) kA[(Tk % ST) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.ak) : -1;
+          else kB[(Tk % ST) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.bk) : -1;
         }
       }
     __syncthreads();
     return T;
   };
 
-  // operand stage Tk of tile T (buffer buf) into ring slot Tk % STAGES
+  // operand stage Tk of tile T (buffer buf) into ring slot Tk % ST
   auto load_stage = [&](const Tile& T, int buf, int Tk) {
     const GemmProblem& P = sP[buf];
     const long long* rowA = tab + buf * TABN;
@@ -207,11 +213,11 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
         const int k = T.kbeg + Tk * BK + kl;
         return k < T.K ? (long long)k * st0 : -1;
       }
-      return ring[(Tk % STAGES) * BK + kl];
+      return ring[(Tk % ST) * BK + kl];
     };
     const cplx* __restrict__ Ag = P.A;
     const cplx* __restrict__ Bg = P.B;
-    const int stage = Tk % STAGES;
+    const int stage = Tk % ST;
     cplx* as = As + stage * C_::A_ELEMS;
     cplx* bs = Bs + stage * C_::B_ELEMS;
     if (!AKM) {   // As[m][k]: k fixed per thread
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
   };
   auto prologue = [&](const Tile& T, int buf) {
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
+    for (int s = 0; s < ST - 1; ++s) {
       if (s < T.ktiles) load_stage(T, buf, s);
       cp_async_commit();
     }
@@ -280,22 +286,22 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped(const GemmProblem* _
         acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
       }
     for (int kt = 0; kt < T.ktiles; ++kt) {
-      cp_async_wait<STAGES - 2>();
+      cp_async_wait<ST - 2>();
       __syncthreads();
-      // decode the k legs of tile kt + STAGES (slot kt % STAGES: its last reader, the load of
+      // decode the k legs of tile kt + ST (slot kt % ST: its last reader, the load of
       // tile kt, was issued before this barrier); visible to the loads after the next barrier
-      if (P.nk != 1 && tid < 2 * BK && kt + STAGES < T.ktiles) {
-        const int Tk = kt + STAGES, kl = tid % BK, k = T.kbeg + Tk * BK + kl;
-        if (tid < BK) kA[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.ak) : -1;
-        else kB[(Tk % STAGES) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.bk) : -1;
+      if (P.nk != 1 && tid < 2 * BK && kt + ST < T.ktiles) {
+        const int Tk = kt + ST, kl = tid % BK, k = T.kbeg + Tk * BK + kl;
+        if (tid < BK) kA[(Tk % ST) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.ak) : -1;
+        else kB[(Tk % ST) * BK + kl] = k < T.K ? goff(k, P.nk, P.kd, P.bk) : -1;
       }
       {
-        const int kn = kt + STAGES - 1;
+        const int kn = kt + ST - 1;
         if (kn < T.ktiles) load_stage(T, buf, kn);
         cp_async_commit();
       }
-      const cplx* as = As + (kt % STAGES) * C_::A_ELEMS;
-      const cplx* bs = Bs + (kt % STAGES) * C_::B_ELEMS;
+      const cplx* as = As + (kt % ST) * C_::A_ELEMS;
+      const cplx* bs = Bs + (kt % ST) * C_::B_ELEMS;
       double ar[BK / 4][TM], ai[BK / 4][TM], nai[BK / 4][TM], br[BK / 4][TN], bi[BK / 4][TN];
 #pragma unroll
       for (int q = 0; q < BK / 4; ++q) {
@@ -471,18 +477,24 @@ int assign_tiles(GemmProblem* h, int n, double& flops, double& bytes) {
   return tiles;
 }
 
+// stages / resident CTAs per SM: the 16-wide skinny tiles are latency-bound (short k loops, few
+// warps), so they trade a pipeline stage for a third resident CTA
+template <int BM, int BN> struct Occ { static constexpr int ST = (BM == 16 || BN == 16) ? TCBC_SKINNY_ST : STAGES, MINB = (BM == 16 || BN == 16) ? TCBC_SKINNY_MINB : 2; };
+
 template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM>
 void launch_variant(const GemmProblem* d, int n, int tiles, cudaStream_t s) {
   if (n == 0 || tiles == 0) return;
-  using C_ = Cfg<BM, BN, AKM, BNM>;
+  constexpr int ST = Occ<BM, BN>::ST, MINB = Occ<BM, BN>::MINB;
+  using C_ = Cfg<BM, BN, AKM, BNM, ST>;
+  static_assert(MINB * C_::BYTES <= 227 * 1024, "shared memory for the resident CTAs");
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C_::BYTES);
+    cudaFuncSetAttribute(zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C_::BYTES);
     attr_done = true;
   }
-  const int grid = std::min(tiles, 2 * 148);   // persistent: two resident CTAs per SM
-  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM><<<grid, THREADS, C_::BYTES, s>>>(d, n, tiles);
+  const int grid = std::min(tiles, MINB * 148);   // persistent: MINB resident CTAs per SM
+  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB><<<grid, THREADS, C_::BYTES, s>>>(d, n, tiles);
   count_launch();
 }
 
