@@ -1147,11 +1147,14 @@ __global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob, i
   if ((what & 1) && P.w_out) *P.w_out = ldexp(*P.w_out, 2 * e);
 }
 
-// K5 for n <= 32 * NQ, one CTA per (matrix, 8 eigenvectors): the eigenvector lives in its
-// warp's registers (lane l owns entries l, l + 32, ...); the reflectors are staged BT_R rows at
-// a time in shared memory by the whole CTA (one coalesced L2 pass shared by 8 vectors), so the
-// sequential sweep reads v_j from shared memory instead of waiting on L2 per reflector.
+// K5 for n <= 32 * NQ, one CTA per (matrix, 8 x VPW eigenvectors): a warp's VPW eigenvectors
+// live in its registers (lane l owns entries l, l + 32, ...); the reflectors are staged BT_R
+// rows at a time in shared memory by the whole CTA (one coalesced L2 pass shared by all its
+// vectors), and each reflector entry read from shared memory serves VPW vectors.
 constexpr int BT_WARPS = 8, BT_R = 16;
+#ifndef BT_VPW
+#define BT_VPW 2   // eigenvectors per warp
+#endif
 __host__ __device__ inline size_t backtr_smem_bytes(int n) { return (size_t)BT_R * n * 16 + BT_R * 16; }
 
 __device__ __forceinline__ int find_bstart(const HeevProblem* p, int n, int b) {
@@ -1163,31 +1166,35 @@ __device__ __forceinline__ int find_bstart(const HeevProblem* p, int n, int b) {
   return lo;
 }
 
-template <int NQ>
+template <int NQ, int VPW>
 __global__ void __launch_bounds__(BT_WARPS * 32) heev_backtr_blk(const HeevProblem* __restrict__ probs, int nprob) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const HeevProblem& P = probs[find_bstart(probs, nprob, blockIdx.x)];
-  const int t0 = (blockIdx.x - P.bstart) * BT_WARPS, t = t0 + warp, n = P.n, kmax = P.kmax;
+  const int t0 = (blockIdx.x - P.bstart) * BT_WARPS * VPW, tw = t0 + warp * VPW, n = P.n, kmax = P.kmax;
   cplx* sv = reinterpret_cast<cplx*>(smem_raw);
   cplx* stau = sv + (size_t)BT_R * n;
   const double* Z = P.work + 2 * n + 8;
   const cplx* A = P.A;
-  cplx* vt = P.Vt + (size_t)t * n;
   const int k = P.k_out ? *P.k_out : kmax;
   if (t0 >= k) {   // block-uniform: every vector of this block is dropped
-    if (t < kmax)
-      for (int i = lane; i < n; i += 32) vt[i] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < VPW; ++u)
+      if (tw + u < kmax)
+        for (int i = lane; i < n; i += 32) P.Vt[(size_t)(tw + u) * n + i] = make_double2(0.0, 0.0);
     return;
   }
-  const bool act = t < k;
-  double yr[NQ], yi[NQ];
+  const bool act = tw < k;   // this warp holds at least one kept vector (dropped ones stay 0)
+  // VPW vectors per warp: each reflector entry read from shared memory serves VPW vectors
+  double yr[VPW][NQ], yi[VPW][NQ];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int i = lane + 32 * q;
-    yr[q] = (act && i < n) ? Z[(size_t)i * kmax + t] : 0.0;
-    yi[q] = 0.0;
-  }
+  for (int u = 0; u < VPW; ++u)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q, t = tw + u;
+      yr[u][q] = (t < k && i < n) ? Z[(size_t)i * kmax + t] : 0.0;
+      yi[u][q] = 0.0;
+    }
   for (int j1 = n - 2; j1 >= 0; j1 -= BT_R) {
     const int j0 = max(0, j1 - BT_R + 1);
     __syncthreads();
@@ -1204,29 +1211,47 @@ __global__ void __launch_bounds__(BT_WARPS * 32) heev_backtr_blk(const HeevProbl
       if (tau.x == 0.0 && tau.y == 0.0) continue;
       const cplx* row = sv + (size_t)(j - j0) * n;
       cplx v[NQ];
-      double sr = 0.0, si = 0.0;   // s = v^H y over i > j (entries i <= j are staged as 0)
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int i = lane + 32 * q;
         v[q] = i < n ? row[i] : make_double2(0.0, 0.0);
-        sr += v[q].x * yr[q] + v[q].y * yi[q];
-        si += v[q].x * yi[q] - v[q].y * yr[q];
       }
-      sr = warp_sum(sr);
-      si = warp_sum(si);
-      const double tr = tau.x * sr - tau.y * si, ti = tau.x * si + tau.y * sr;
+      double sr[VPW], si[VPW];   // s = v^H y over i > j (entries i <= j are staged as 0)
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        yr[q] -= tr * v[q].x - ti * v[q].y;
-        yi[q] -= tr * v[q].y + ti * v[q].x;
+      for (int u = 0; u < VPW; ++u) {
+        sr[u] = 0.0;
+        si[u] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          sr[u] += v[q].x * yr[u][q] + v[q].y * yi[u][q];
+          si[u] += v[q].x * yi[u][q] - v[q].y * yr[u][q];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < VPW; ++u) {
+        sr[u] = warp_sum(sr[u]);
+        si[u] = warp_sum(si[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < VPW; ++u) {
+        const double tr = tau.x * sr[u] - tau.y * si[u], ti = tau.x * si[u] + tau.y * sr[u];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          yr[u][q] -= tr * v[q].x - ti * v[q].y;
+          yi[u][q] -= tr * v[q].y + ti * v[q].x;
+        }
       }
     }
   }
-  if (t >= kmax) return;
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int i = lane + 32 * q;
-    if (i < n) vt[i] = make_double2(yr[q], yi[q]);
+  for (int u = 0; u < VPW; ++u) {
+    const int t = tw + u;
+    if (t >= kmax) continue;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      if (i < n) P.Vt[(size_t)t * n + i] = make_double2(yr[u][q], yi[u][q]);
+    }
   }
 }
 
@@ -1469,7 +1494,7 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::f
     h[i].estart = total;
     total += h[i].kmax;
     h[i].bstart = nblk;
-    nblk += (h[i].kmax + BT_WARPS - 1) / BT_WARPS;
+    nblk += (h[i].kmax + BT_WARPS * BT_VPW - 1) / (BT_WARPS * BT_VPW);
     const double nn = h[i].n;
     fl += 8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * h[i].kmax);
     by += 16.0 * nn * nn;
@@ -1568,12 +1593,14 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::f
     if (mxn <= 256) {
       static bool battr = false;
       if (!battr) {
-        cudaFuncSetAttribute(heev_backtr_blk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
-        cudaFuncSetAttribute(heev_backtr_blk<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
+        cudaFuncSetAttribute(heev_backtr_blk<4, BT_VPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
+        cudaFuncSetAttribute(heev_backtr_blk<6, BT_VPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
+        cudaFuncSetAttribute(heev_backtr_blk<8, BT_VPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
         battr = true;
       }
-      if (mxn <= 128) heev_backtr_blk<4><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
-      else heev_backtr_blk<8><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
+      if (mxn <= 128) heev_backtr_blk<4, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
+      else if (mxn <= 192) heev_backtr_blk<6, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
+      else heev_backtr_blk<8, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
     } else {
       heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
     }
