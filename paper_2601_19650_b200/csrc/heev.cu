@@ -248,21 +248,27 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
         const bool in = c <= r;
         const int cc = in ? c : r;   // in-range index for the vector reads
         cplx av = a[q];
-        if (have_prev) {
+        if (have_prev) {   // a -= v_r conj(w_c) + w_r conj(v_c): one FMA chain per component
           const cplx vpc = vprev[cc], wpc = wprev[cc];
-          av.x -= (vpr.x * wpc.x + vpr.y * wpc.y) + (wpr.x * vpc.x + wpr.y * vpc.y);
-          av.y -= (vpr.y * wpc.x - vpr.x * wpc.y) + (wpr.y * vpc.x - wpr.x * vpc.y);
+          av.x = fma(-vpr.x, wpc.x, av.x);
+          av.x = fma(-vpr.y, wpc.y, av.x);
+          av.x = fma(-wpr.x, vpc.x, av.x);
+          av.x = fma(-wpr.y, vpc.y, av.x);
+          av.y = fma(-vpr.y, wpc.x, av.y);
+          av.y = fma(vpr.x, wpc.y, av.y);
+          av.y = fma(-wpr.y, vpc.x, av.y);
+          av.y = fma(wpr.x, vpc.y, av.y);
           if (in) rowp[c] = av;
           av.x = in ? av.x : 0.0;
           av.y = in ? av.y : 0.0;
         }
         const cplx vc = vcur[cc];
-        sr += av.x * vc.x - av.y * vc.y;
-        si += av.x * vc.y + av.y * vc.x;
+        sr = fma(av.x, vc.x, fma(-av.y, vc.y, sr));
+        si = fma(av.x, vc.y, fma(av.y, vc.x, si));
         // (r, c) also stands for A[c][r] = conj(a): p[c] += conj(a) v_r (strictly below the diagonal)
         const double wx = c < r ? vr.x : 0.0, wy = c < r ? vr.y : 0.0;
-        cacc[q].x += av.x * wx + av.y * wy;
-        cacc[q].y += av.x * wy - av.y * wx;
+        cacc[q].x = fma(av.x, wx, fma(av.y, wy, cacc[q].x));
+        cacc[q].y = fma(av.x, wy, fma(-av.y, wx, cacc[q].y));
       }
       sr = warp_sum(sr);
       si = warp_sum(si);
