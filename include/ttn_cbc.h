@@ -113,6 +113,11 @@ TTN_API ttn_status ttn_get_tensor(ttn_ctx ctx, ttn t, int32_t node, ttn_c128* ho
 /* Copy every node (node 0 first, each in ABI leg order, concatenated) to host memory with
  * one D2H copy; capacity_elems must cover the sum of the node sizes.  Synchronises.     */
 TTN_API ttn_status ttn_get_data(ttn_ctx ctx, ttn t, ttn_c128* host_out, size_t capacity_elems);
+/* ttn_get_data for n TTNs (host_out[i], capacity_elems[i]): all D2H copies are enqueued,
+ * then the ctx stream is synchronised once.  Pinned host buffers let the copies run at
+ * full link speed.  ARG if any buffer is too small (nothing copied then).                */
+TTN_API ttn_status ttn_get_data_batch(ttn_ctx ctx, int32_t n, const ttn* t, ttn_c128* const* host_out,
+                                      const size_t* capacity_elems);
 
 /* ---------------------------------------------------------------- CBC                  */
 /* phi ~= O |psi> by CBC (§III.B, Eqs. 10-14; tensor train §III.A,

@@ -16,7 +16,7 @@ from . import _lib as L
 from ._lib import TTN_OPERATOR, TTN_STATE, TTNError
 
 __all__ = ["Context", "TTN", "ttn_ctx_create", "ttn_create", "cbc_apply", "cbc_apply_batch", "ttn_overlap",
-           "ttn_overlap_batch", "ttn_norm", "ttn_get_tensor", "ttn_version", "TTN_STATE", "TTN_OPERATOR",
+           "ttn_overlap_batch", "ttn_norm", "ttn_get_tensor", "ttn_get_data", "ttn_get_data_batch", "ttn_version", "TTN_STATE", "TTN_OPERATOR",
            "TTNError", "lib_path"]
 
 lib_path = L.LIB_PATH
@@ -130,6 +130,19 @@ def ttn_get_tensor(ctx: Context, t: TTN, node: int) -> np.ndarray:
     out = np.empty(shp, dtype=np.complex128)
     L.check(ctx.h, L.load().ttn_get_tensor(ctx.h, t.h, node, C.c_void_p(out.ctypes.data), out.size))
     return out
+
+
+def ttn_get_data_batch(ctx: Context, ts, outs):
+    """ttn_get_data for several TTNs into the given buffers (numpy complex128 or pinned torch
+    complex128 CPU tensors); one stream synchronisation for all copies."""
+    n = len(ts)
+    if len(outs) != n:
+        raise ValueError("one output buffer per TTN")
+    hs = (C.c_void_p * n)(*[t.h for t in ts])
+    ptrs = (C.c_void_p * n)(*[(o.data_ptr() if hasattr(o, "data_ptr") else o.ctypes.data) for o in outs])
+    caps = (C.c_size_t * n)(*[(o.numel() if hasattr(o, "numel") else o.size) for o in outs])
+    L.check(ctx.h, L.load().ttn_get_data_batch(ctx.h, n, hs, ptrs, caps))
+    return outs
 
 
 def ttn_get_data(ctx: Context, t: TTN, out=None):

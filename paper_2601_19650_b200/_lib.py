@@ -20,7 +20,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_TOPOLOGY", 3: "ERR_SHAPE", 4: "ERR_OOM"
 # the C ABI symbols (kept in sync with include/ttn_cbc.h; tests/test_abi.py checks both)
 SYMBOLS = ["ttn_ctx_create", "ttn_ctx_destroy", "ttn_last_error", "ttn_version", "ttn_create", "ttn_destroy",
            "ttn_n_nodes", "ttn_node_shape", "ttn_get_tensor", "cbc_apply", "cbc_apply_batch", "ttn_overlap",
-           "ttn_overlap_batch", "ttn_norm", "ttn_get_data", "ttn_profile_enable", "ttn_profile_read", "ttn_launch_count",
+           "ttn_overlap_batch", "ttn_norm", "ttn_get_data", "ttn_get_data_batch", "ttn_profile_enable", "ttn_profile_read", "ttn_launch_count",
            "ttn_comm_unique_id", "ttn_ctx_set_comm", "ttn_partition_plan", "ttn_ctx_set_workers",
            "ttn_sandwich", "ttn_op_norm2"]
 
@@ -74,6 +74,7 @@ def load():
         "ttn_overlap_batch": (C.c_int, [P, I32, C.POINTER(P), C.POINTER(P), C.POINTER(c128)]),
         "ttn_norm": (C.c_int, [P, P, C.POINTER(D)]),
         "ttn_get_data": (C.c_int, [P, P, P, C.c_size_t]),
+        "ttn_get_data_batch": (C.c_int, [P, I32, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_size_t)]),
         "ttn_profile_enable": (C.c_int, [C.c_int]),
         "ttn_profile_read": (C.c_int, [C.c_char_p, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I64)]),
         "ttn_launch_count": (C.c_int, [C.POINTER(I64)]),

@@ -204,6 +204,22 @@ ttn_status ttn_get_data(ttn_ctx ctx, ttn t, ttn_c128* host_out, size_t capacity_
   });
 }
 
+ttn_status ttn_get_data_batch(ttn_ctx ctx, int32_t n, const ttn* t, ttn_c128* const* host_out,
+                              const size_t* capacity_elems) {
+  if (!ctx || n < 0 || (n > 0 && (!t || !host_out || !capacity_elems))) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    for (int i = 0; i < n; ++i) {
+      if (!t[i] || !host_out[i]) throw Error(TTN_ERR_ARG, "NULL handle or buffer");
+      if ((size_t)t[i]->total > capacity_elems[i]) throw Error(TTN_ERR_ARG, "output buffer too small");
+    }
+    for (int i = 0; i < n; ++i)
+      TTN_CUDA(cudaMemcpyAsync(host_out[i], t[i]->data, sizeof(cplx) * t[i]->total, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    ctx->sync();
+  });
+}
+
 ttn_status cbc_apply(ttn_ctx ctx, ttn op, ttn state, int64_t max_bond, double tol, ttn* out, ttn_cbc_report* rep) {
   if (!ctx || !out) return TTN_ERR_ARG;
   return cbc_apply_batch(ctx, 1, &op, &state, max_bond, tol, out, rep);

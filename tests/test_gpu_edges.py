@@ -121,3 +121,22 @@ def test_worker_subbatches_match_single_stream(P, ctx):
         for tx, ty in zip(x.tensors, y.tensors):
             assert np.allclose(tx, ty, rtol=0, atol=1e-12 * max(1.0, np.abs(ty).max()))
         assert abs(ra["norm"] - rb["norm"]) <= 1e-12 * rb["norm"]
+
+
+def test_get_data_batch_matches_per_tensor_reads(P, ctx):
+    """ttn_get_data_batch (one synchronisation) returns what ttn_get_tensor returns node by
+    node, and refuses a buffer that is too small."""
+    parent = W.complete_binary(7)
+    insts = [W.configs.random_instance(parent, [2] * 7, 3, 2, 4, seed=70 + s) for s in range(3)]
+    outs = []
+    for i in insts:
+        op_g, st_g = gpu_pair(P, ctx, i)
+        outs.append(P.cbc_apply(ctx, op_g, st_g, i.max_bond)[0])
+    sizes = [sum(int(np.prod(o.shape(q))) for q in range(o.n_nodes)) for o in outs]
+    bufs = [np.empty(sz, dtype=np.complex128) for sz in sizes]
+    P.ttn_get_data_batch(ctx, outs, bufs)
+    for o, b in zip(outs, bufs):
+        ref = np.concatenate([P.ttn_get_tensor(ctx, o, q).ravel() for q in range(o.n_nodes)])
+        assert np.array_equal(b, ref)
+    with pytest.raises(P.TTNError):
+        P.ttn_get_data_batch(ctx, outs, [np.empty(sizes[0] - 1, dtype=np.complex128)] + bufs[1:])

@@ -19,7 +19,7 @@ def packed(tensors):
 hs = [packed(i.state) for i in insts]
 ho = [packed(i.op) for i in insts]
 parent, phys, mb = insts[0].parent, insts[0].phys, 32
-for rep in range(3):
+for rep in range(8):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     st = [P.ttn_create(ctx, P.TTN_STATE, parent, phys, i.state_bond, ts) for i, ts in zip(insts, hs)]
     op = [P.ttn_create(ctx, P.TTN_OPERATOR, parent, phys, i.op_bond, ts) for i, ts in zip(insts, ho)]
