@@ -444,9 +444,10 @@ def run_native(args, rank, world, local_rank):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": batch * world * n_e2e / (te.item() / 1000.0), "unit": "applies/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "note": "ttn_create from one pinned host buffer per TTN + cbc_apply_batch + ttn_get_data into pinned "
-                       "host memory, two pipelined lanes (contexts / streams / host threads) so copies of one "
-                       "batch overlap the other's compute; CUDA events around the whole sequence, max over ranks"}
+               "note": "ttn_create from one pinned host buffer per TTN + cbc_apply_batch + ttn_get_data_batch into "
+                       "pinned host memory, every step; two lanes (contexts / streams / host threads) run out of "
+                       "phase so one batch's copies overlap the other's compute; CUDA events around the whole "
+                       "sequence, max over ranks"}
 
     if rank != 0:
         ctx.close()

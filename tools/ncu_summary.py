@@ -30,14 +30,17 @@ def launches(src, dst):
     rows = [r for r in csv.reader(open(src)) if len(r) > 10]
     h = rows[0]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = 0.0
     for r in rows[1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         try:
             v = float(r[vi].replace(",", ""))
         except ValueError:
             continue
-        name = r[ki].split("(")[0].replace("void ", "").replace("unnamed>::", "")
+        name = r[ki].split("(")[0].replace("void ", "").replace("tcbc::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
         agg[name][0] += 1
         agg[name][1] += v
         tot += v
@@ -90,7 +93,7 @@ def traffic(src, dst_md, dst_json, applies=2):
         except ValueError:
             continue
         per[r[idk]][r[mi]] = v
-        per[r[idk]]["name"] = r[ki].split("(")[0]
+        per[r[idk]]["name"] = r[ki].split("(")[0].replace("tcbc::", "").replace("<unnamed>::", "")
     launches = [d for d in per.values() if "dram__bytes_read.sum" in d and "zgemm_grouped" in d["name"]]
     tot_b = sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in launches)
     tot_t = sum(d.get("gpu__time_duration.sum", 0.0) for d in launches)
