@@ -131,11 +131,18 @@ constexpr int SMEM_MAX_N = 144;    // matrix (packed lower triangle) resident in
 // triangle with two CTAs per SM beats the fully resident one with one CTA per SM (heev
 // 28 -> 26 ms per step).
 constexpr size_t FUSED_SMEM_BUDGET = 110u << 10;
+// n <= 128 (NQ = 4: 80 registers) fits three CTAs per SM by registers; their budget keeps three
+#ifndef TCBC_SMALL_BUDGET_KB
+#define TCBC_SMALL_BUDGET_KB 72
+#endif
+__host__ __device__ inline size_t fused_budget(int n) {
+  return n <= 128 ? ((size_t)TCBC_SMALL_BUDGET_KB << 10) : FUSED_SMEM_BUDGET;
+}
 __host__ __device__ inline size_t fused_base_bytes(int n) { return (size_t)n * 16 * 2 + (size_t)16 * (3 + 8) * n + 64; }
 // n = 192 (config 3's G-route Grams): the last ~25 rows fit; heev 26 -> 25 ms per step.
 __host__ __device__ inline int fused_r0(int n) {
   if (n > FUSED_MAX_N) return n;
-  const size_t avail = (FUSED_SMEM_BUDGET - fused_base_bytes(n)) / 16;   // complex entries
+  const size_t avail = (fused_budget(n) - fused_base_bytes(n)) / 16;   // complex entries
   int r0 = 0;
   while ((size_t)n * (n + 1) / 2 - (size_t)r0 * (r0 + 1) / 2 > avail) ++r0;
   return r0;
@@ -464,8 +471,12 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* 
   double tr = 0.0;
   for (int i = tid; i < n; i += HEEV_THREADS) tr += A[(size_t)i * n + i].x;
   const double trace = block_sum2(tr, 0.0, red).x;
-  if (n <= 32 * NQ) tridiag_fused<NQ>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
-  else tridiag_full(A, n, sv, sp, dvec, evec, P.tau, red);
+  if constexpr (NQ == 8) {   // the launcher sends n > 192 only to this instantiation
+    if (n <= 32 * NQ) tridiag_fused<NQ>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
+    else tridiag_full(A, n, sv, sp, dvec, evec, P.tau, red);
+  } else {
+    tridiag_fused<NQ>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
+  }
   tridiag_stats(P, trace);
 }
 
