@@ -379,6 +379,30 @@ __global__ void __launch_bounds__(THREADS, MINB) zgemm_grouped(const GemmProblem
               if (n < N) W[(size_t)m * N + n] = make_double2(acc_re[i][j][h], acc_im[i][j][h]);
             }
         }
+      } else if (T.m0 + BM <= M && T.n0 + BN <= N && al.x == 1.0 && al.y == 0.0 && !use_beta && !T.mirror) {
+        // common case (uniform branch): full tile, C = A B -- no bounds, scaling or mirror work
+        const bool ex = P.exp_out != nullptr;
+        long long co[TN][2];
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) co[j][h] = colC[wn + j * 8 + fc * 2 + h];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          cplx* crow = Cg + rowC[wm + i * 8 + fr];
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double re = acc_re[i][j][h], im = acc_im[i][j][h];
+              crow[co[j][h]] = make_double2(re, im);
+              if (ex) emax = max(emax, max(bexp(re), bexp(im)));
+            }
+        }
+        if (ex) {
+          for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+          if (lane == 0 && emax > -2147483000) atomicMax(P.exp_out, emax);
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
