@@ -1555,9 +1555,9 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::f
     else heev_tridiag<8><<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
     count_launch();
   }
-  {   // smallest lanes-per-eigenvalue that still keeps ~12 warps per SM busy
+  {   // smallest lanes-per-eigenvalue that still keeps ~6 warps per SM busy
     int G = 1;
-    while (G < 32 && (long long)total * G < 148LL * 12 * 32) G *= 2;
+    while (G < 32 && (long long)total * G < 148LL * 6 * 32) G *= 2;   // measured: 6 beats 3, 12, 24
     const int blocks = (int)(((long long)total * G + 255) / 256);
     switch (G) {
       case 1: heev_bisect<1><<<blocks, 256, 0, s>>>(d, n, total); break;
