@@ -180,6 +180,13 @@ void launch_fill(cplx* p, long long n, cplx v, cudaStream_t s) {
   count_launch();
 }
 
+// blocks per problem: ~16 blocks per SM in total, at least one per problem (most problems have
+// a zero exponent and their blocks exit at once, so many idle blocks only cost scheduling)
+static unsigned pow2_gx(long long mx, int n) {
+  const long long per = std::max<long long>(1, (148LL * 16) / std::max(n, 1));
+  return (unsigned)std::max<long long>(1, std::min<long long>((mx + 255) / 256, per));
+}
+
 void launch_pow2_normalize(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   long long mx = 1;
@@ -195,7 +202,7 @@ void launch_pow2_normalize(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
   const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
   const unsigned gx = (unsigned)std::min<long long>((mx + 255) / 256, 296);
   pow2_maxexp<<<dim3(gx, n), 256, 0, s>>>(d);
-  pow2_scale<<<dim3(gx, n), 256, 0, s>>>(d, -1);
+  pow2_scale<<<dim3(pow2_gx(mx, n), n), 256, 0, s>>>(d, -1);
   count_launch();
   count_launch();
 }
@@ -205,8 +212,7 @@ void launch_pow2_restore(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
   long long mx = 1;
   for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].len);
   const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
-  const unsigned gx = (unsigned)std::min<long long>((mx + 255) / 256, 296);
-  pow2_scale<<<dim3(gx, n), 256, 0, s>>>(d, +1);
+  pow2_scale<<<dim3(pow2_gx(mx, n), n), 256, 0, s>>>(d, +1);
   count_launch();
 }
 
@@ -215,8 +221,7 @@ void launch_pow2_apply(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
   long long mx = 1;
   for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].len);
   const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
-  const unsigned gx = (unsigned)std::min<long long>((mx + 255) / 256, 296);
-  pow2_scale<<<dim3(gx, n), 256, 0, s>>>(d, -1);
+  pow2_scale<<<dim3(pow2_gx(mx, n), n), 256, 0, s>>>(d, -1);
   count_launch();
 }
 
