@@ -561,6 +561,7 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
   grp.assign(n, 255);
   int cnt[NV] = {0};
   int nsplit = 0, total = 0;
+  int memo_m = -1, memo_n = -1, memo_k = -1, memo_best = 0;
   for (int i = 0; i < n; ++i) {
     GemmProblem& p = h[i];
     if (p.M <= 0 || p.N <= 0) continue;
@@ -571,11 +572,19 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
     const bool bnm = (p.bn[p.nn - 1] != 1) && (p.bk[p.nk - 1] == 1);
     const int v = (akm ? 2 : 0) + (bnm ? 1 : 0);
     int best = 0;
-    if (!p.sym) {
-      double bc = shape_cost(p, kShapes[0]);
-      for (int t = 1; t < kNumShapes; ++t) {
-        const double c = shape_cost(p, kShapes[t]);
-        if (c < bc * 0.999) { bc = c; best = t; }
+    if (!p.sym) {   // consecutive problems mostly share a shape (one plan step over the batch)
+      if (p.M == memo_m && p.N == memo_n && p.K == memo_k) {
+        best = memo_best;
+      } else {
+        double bc = shape_cost(p, kShapes[0]);
+        for (int t = 1; t < kNumShapes; ++t) {
+          const double c = shape_cost(p, kShapes[t]);
+          if (c < bc * 0.999) { bc = c; best = t; }
+        }
+        memo_m = p.M;
+        memo_n = p.N;
+        memo_k = p.K;
+        memo_best = best;
       }
     }
     p.ksplit = 1;
