@@ -209,6 +209,10 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   if (early) {
     ctx->wait_ranks();
   } else {
+    // the Chebyshev solver may have grown (reallocated) the small pinned buffer: re-derive
+    ctx->ensure_small(sizeof(int) * nj + sizeof(double) * nj);
+    hk = reinterpret_cast<int*>(ctx->hbuf);
+    hw = reinterpret_cast<double*>(ctx->hbuf + sizeof(int) * ((nj + 1) & ~1));
     read_ranks();
     ctx->sync();
   }
