@@ -181,6 +181,123 @@ __global__ void __launch_bounds__(CH_THREADS) potrf_grouped(const PotrfProblem* 
   if (tid == 0 && P.info) *P.info = s_fail;
 }
 
+// Small orders (n <= 64, config 2's CholeskyQR Grams of order 64): the whole matrix in shared
+// memory, unblocked right-looking Cholesky (two barriers per column) -- a sequential chain of
+// 64 short steps instead of four panels of staged blocks.  Same outputs and info as above.
+constexpr int CH_SMALL = 64;
+
+__global__ void __launch_bounds__(256) potrf_small(const PotrfProblem* __restrict__ probs) {
+  const PotrfProblem P = probs[blockIdx.x];
+  const int n = P.n, ldS = n + 1;
+  const long long ld = P.lda;
+  cplx* A = P.A;
+  extern __shared__ __align__(16) unsigned char ch_smem[];
+  cplx* S = reinterpret_cast<cplx*>(ch_smem);   // [n][n + 1], lower triangle used
+  __shared__ double red[32];
+  __shared__ int s_fail;
+  const int tid = threadIdx.x;
+  double md = -1e300;
+  for (int e = tid; e < n * n; e += 256) {
+    const int r = e / n, c = e % n;
+    if (c <= r) {
+      const cplx v = A[r * ld + c];
+      S[r * ldS + c] = v;
+      if (c == r) md = fmax(md, v.x);
+    }
+  }
+  md = block_max(md, red);   // (its barriers also publish S)
+  if (P.shift_rel > 0.0 && md > 0.0) {
+    const double sh = P.shift_rel * md;
+    for (int i = tid; i < n; i += 256) S[i * ldS + i].x += sh;
+    md += sh;
+  }
+  const double thresh = P.rel_tol * md;
+  if (tid == 0) s_fail = (md > 0.0 && isfinite(md)) ? 0 : 1;
+  __syncthreads();
+  for (int c = 0; c < n && !s_fail; ++c) {
+    const double d = S[c * ldS + c].x;
+    if (!(d > thresh) || !isfinite(d)) {   // uniform: every thread reads the same pivot
+      if (tid == 0) s_fail = c + 1;
+      break;
+    }
+    const double sd = sqrt(d), inv = 1.0 / sd;
+    for (int r = c + 1 + tid; r < n; r += 256) {
+      const cplx v = S[r * ldS + c];
+      S[r * ldS + c] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncthreads();
+    if (tid == 0) S[c * ldS + c] = make_double2(sd, 0.0);
+    // A22 -= l l^H (lower part): 16 x 16 thread grid over (row, column), no index division
+    for (int r = c + 1 + (tid >> 4); r < n; r += 16) {
+      const cplx lr = S[r * ldS + c];
+      for (int l = c + 1 + (tid & 15); l <= r; l += 16) {
+        const cplx u = cmulc(lr, S[l * ldS + c]);
+        S[r * ldS + l].x -= u.x;
+        S[r * ldS + l].y -= u.y;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (!s_fail) {
+    for (int e = tid; e < n * n; e += 256) {
+      const int r = e / n, c = e % n;
+      A[r * ld + c] = c <= r ? S[r * ldS + c] : make_double2(0.0, 0.0);
+    }
+  }
+  if (tid == 0 && P.info) *P.info = s_fail;
+}
+
+// Linv = L^{-1} for n <= 64: L in shared memory, four lanes per column of Linv (forward
+// substitution down the column, the column's inner products split over the four lanes and
+// combined by shuffles; diagonal reciprocals precomputed).
+__global__ void __launch_bounds__(4 * CH_SMALL) trtri_small(const TrtriProblem* __restrict__ probs) {
+  const TrtriProblem P = probs[blockIdx.x];
+  const int n = P.n, ldS = n + 1;
+  const long long ld = P.ld;
+  extern __shared__ __align__(16) unsigned char ch_smem[];
+  cplx* L = reinterpret_cast<cplx*>(ch_smem);   // [n][n + 1]
+  cplx* X = L + (size_t)n * ldS;                // [n][n + 1]: X[a][b] = Linv[a][b]
+  cplx* R = X + (size_t)n * ldS;                // [n]: 1 / L[a][a]
+  const int tid = threadIdx.x, b = tid >> 2, sub = tid & 3;
+  for (int e = tid; e < n * n; e += 4 * CH_SMALL) {
+    const int r = e / n, c = e % n;
+    if (c <= r) L[r * ldS + c] = P.L[r * ld + c];
+  }
+  __syncthreads();
+  for (int a = tid; a < n; a += 4 * CH_SMALL) R[a] = cdiv(make_double2(1.0, 0.0), L[a * ldS + a]);
+  __syncthreads();
+  // a warp holds columns b0 .. b0 + 7; all its lanes run the same rows a >= b0 (the shuffles
+  // need every lane), a lane contributing only once a >= its own column
+  const int b0 = (tid >> 5) * 8;
+  if (b0 < n) {
+    if (sub == 0 && b < n)
+      for (int a = 0; a < b; ++a) X[a * ldS + b] = make_double2(0.0, 0.0);
+    __syncwarp();
+    for (int a = b0; a < n; ++a) {
+      const bool act = b < n && a >= b;
+      double sr = 0.0, si = 0.0;
+      if (act)
+        for (int j = b + sub; j < a; j += 4) {
+          const cplx u = cmul(L[a * ldS + j], X[j * ldS + b]);
+          sr += u.x;
+          si += u.y;
+        }
+      sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+      si += __shfl_xor_sync(0xffffffffu, si, 1);
+      sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+      si += __shfl_xor_sync(0xffffffffu, si, 2);
+      if (act && sub == 0) X[a * ldS + b] = cmul(make_double2((a == b ? 1.0 : 0.0) - sr, -si), R[a]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += 4 * CH_SMALL) {
+    const int r = e / n, c = e % n;
+    P.Linv[r * ld + c] = X[r * ldS + c];
+  }
+}
+
 // Blocked triangular inverse Linv = L^{-1} (lower), by 16-row blocks top to bottom: the block's
 // rows of L are staged in shared memory, one warp inverts the 16 x 16 diagonal block D, and
 // every column c < R0 is formed as  Linv[R, c] = -D^{-1} sum_{j in [c, R0)} L[R, j] Linv[j, c]
@@ -384,7 +501,18 @@ void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s) {
     attr = smem;
   }
   prof_begin(s);
-  potrf_grouped<<<n, CH_THREADS, smem, s>>>(d);
+  if (mx <= CH_SMALL) {
+    const size_t sm = (size_t)mx * (mx + 1) * sizeof(cplx);
+    static bool sattr = false;
+    if (!sattr) {
+      cudaFuncSetAttribute(potrf_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((size_t)CH_SMALL * (CH_SMALL + 1) * sizeof(cplx)));
+      sattr = true;
+    }
+    potrf_small<<<n, 256, sm, s>>>(d);
+  } else {
+    potrf_grouped<<<n, CH_THREADS, smem, s>>>(d);
+  }
   prof_end(s, "potrf", fl, 0.0);
   count_launch();
 }
@@ -403,7 +531,18 @@ void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s) {
     attr = smem;
   }
   prof_begin(s);
-  trtri_grouped<<<n, CH_THREADS, smem, s>>>(d);
+  if (mx <= CH_SMALL) {
+    const size_t sm = (2 * (size_t)mx * (mx + 1) + mx) * sizeof(cplx);
+    static bool sattr = false;
+    if (!sattr) {
+      cudaFuncSetAttribute(trtri_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((2 * (size_t)CH_SMALL * (CH_SMALL + 1) + CH_SMALL) * sizeof(cplx)));
+      sattr = true;
+    }
+    trtri_small<<<n, 4 * CH_SMALL, sm, s>>>(d);
+  } else {
+    trtri_grouped<<<n, CH_THREADS, smem, s>>>(d);
+  }
   prof_end(s, "trtri", fl, 0.0);
   count_launch();
 }
