@@ -514,7 +514,8 @@ __global__ void __launch_bounds__(CL_THREADS) heev_tridiag_cluster(const HeevPro
   cplx* vw = pv + n;                                 // v then w (local)        [n]
   double2* partN = reinterpret_cast<double2*>(vw + n);   // [16]
   double2* partD = partN + 16;                            // [16]
-  __shared__ double2 red[NW + 1];
+  __shared__ double2 red[2 * NW + 1];
+  static_assert(NW == HEEV_WARPS, "one-barrier reductions assume HEEV_WARPS warps");
   __shared__ cplx s_v[1];
   double* dvec = P.work;
   double* evec = P.work + n;
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(CL_THREADS) heev_tridiag_cluster(const HeevPro
       for (int d = 0; d < CS; ++d) *cl.map_shared_rank(x + i, d) = xi;
     }
     if (j >= r0 && j < r1 && tid == 0) dvec[j] = rows[(size_t)(j - r0) * n + j].x;
-    pn = block_sum2(pn, 0.0, red).x;
+    pn = block_sum2_1b(pn, 0.0, red, 0).x;
     if (tid < CS) *cl.map_shared_rank(partN + rank, tid) = make_double2(pn, 0.0);
     cl.sync();
     double xn2 = 0.0;
@@ -599,7 +600,7 @@ __global__ void __launch_bounds__(CL_THREADS) heev_tridiag_cluster(const HeevPro
     dr = __shfl_sync(0xffffffffu, dr, 0);
     di = __shfl_sync(0xffffffffu, di, 0);
     if (lane != 0) { dr = 0.0; di = 0.0; }
-    const double2 dl = block_sum2(dr, di, red);
+    const double2 dl = block_sum2_1b(dr, di, red, 1);
     if (tid < CS) *cl.map_shared_rank(partD + rank, tid) = dl;
     cl.sync();
     double2 dot = make_double2(0.0, 0.0);
