@@ -176,28 +176,33 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
   cplx a2_prev = make_double2(0.0, 0.0);
   for (int j = 0; j < n - 1; ++j) {
     // (a) pending update U_{j-1} on column j (rows >= j), fused with (b)'s |x|^2 partials:
-    // each thread sums the entries it just updated, so the only barrier is the reduction's
+    // thread t owns row j + t of the column (n <= FUSED_MAX_N <= HEEV_THREADS) and keeps the
+    // updated entry in a register for the reflector, so the only barrier is the reduction's
+    // and the column is not read back from memory
+    static_assert(FUSED_MAX_N <= HEEV_THREADS, "one column entry per thread");
+    __shared__ cplx s_alpha;
     double part = 0.0;
-    {
+    const int rj = j + tid;
+    cplx xj = make_double2(0.0, 0.0);
+    if (rj < n) {
       // pivot entries of U_{j-1} from data every thread can see (vcur[j] from step j-1's
       // reflector, wcur[j] from before its reduction barrier), not another thread's vprev / wprev
-      const cplx vpj = vcur[j], wq = wcur[j];
-      const cplx wpj = make_double2(wq.x + a2_prev.x * vpj.x - a2_prev.y * vpj.y,
-                                    wq.y + a2_prev.x * vpj.y + a2_prev.y * vpj.x);
-      for (int r = j + tid; r < n; r += HEEV_THREADS) {
-        cplx a = LL(r, j);
-        if (have_prev) {
-          const cplx vr = vprev[r], wr = wprev[r];
-          a.x -= (vr.x * wpj.x + vr.y * wpj.y) + (wr.x * vpj.x + wr.y * vpj.y);
-          a.y -= (vr.y * wpj.x - vr.x * wpj.y) + (wr.y * vpj.x - wr.x * vpj.y);
-          LL(r, j) = a;
-        }
-        if (r >= j + 2) part += a.x * a.x + a.y * a.y;
+      xj = LL(rj, j);
+      if (have_prev) {
+        const cplx vpj = vcur[j], wq = wcur[j];
+        const cplx wpj = make_double2(wq.x + a2_prev.x * vpj.x - a2_prev.y * vpj.y,
+                                      wq.y + a2_prev.x * vpj.y + a2_prev.y * vpj.x);
+        const cplx vr = vprev[rj], wr = wprev[rj];
+        xj.x -= (vr.x * wpj.x + vr.y * wpj.y) + (wr.x * vpj.x + wr.y * vpj.y);
+        xj.y -= (vr.y * wpj.x - vr.x * wpj.y) + (wr.y * vpj.x - wr.x * vpj.y);
+        LL(rj, j) = xj;
       }
+      if (rj >= j + 2) part = xj.x * xj.x + xj.y * xj.y;
+      if (rj == j + 1) s_alpha = xj;
     }
     // (b) reflector H_j from x = A[j+1:, j]  (zlarfg)
     const double xn2 = block_sum2_1b(part, 0.0, red, 0).x;
-    const cplx alpha = LL(j + 1, j);
+    const cplx alpha = s_alpha;
     double beta;
     cplx tau, scale;
     if (xn2 == 0.0 && alpha.y == 0.0) {
@@ -212,19 +217,15 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
       scale = make_double2(den.x / dd, -den.y / dd);
     }
     const bool tnz = (tau.x != 0.0 || tau.y != 0.0);
-    for (int r = j + 1 + tid; r < n; r += HEEV_THREADS) {
-      cplx v;
-      if (r == j + 1) v = make_double2(1.0, 0.0);
-      else {
-        const cplx x = LL(r, j);
-        v = make_double2(x.x * scale.x - x.y * scale.y, x.x * scale.y + x.y * scale.x);
-      }
-      A[(size_t)j * n + r] = v;                        // kept for the back-transform
-      vcur[r] = tnz ? v : make_double2(0.0, 0.0);
+    if (rj > j && rj < n) {
+      const cplx v = rj == j + 1 ? make_double2(1.0, 0.0)
+                                 : make_double2(xj.x * scale.x - xj.y * scale.y, xj.x * scale.y + xj.y * scale.x);
+      A[(size_t)j * n + rj] = v;                        // kept for the back-transform
+      vcur[rj] = tnz ? v : make_double2(0.0, 0.0);
     }
     if (tid == 0) {
       evec[j] = beta;
-      dvec[j] = LL(j, j).x;
+      dvec[j] = xj.x;   // row j is thread 0's
       tau_out[j] = tau;
     }
     __syncthreads();
