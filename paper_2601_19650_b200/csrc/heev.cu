@@ -235,7 +235,9 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
     cplx cacc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) cacc[q] = make_double2(0.0, 0.0);
-    for (int r = j + 1 + warp; r < n; r += HEEV_WARPS) {
+    // the row's contribution (update of U_{j-1}, its dot with v_j, the column partials) without
+    // the cross-lane reduction of the dot
+    auto row_partial = [&](const int r, double& sr, double& si) {
       const int nq = (r - j + 31) >> 5;   // column blocks that reach the diagonal (warp-uniform)
       // the row's storage (shared-memory tail or global), as one generic pointer: no per-entry
       // branch; entries past the diagonal are masked by selects, not branches
@@ -248,7 +250,6 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
       }
       const cplx vr = vcur[r];
       const cplx vpr = vprev[r], wpr = wprev[r];
-      double sr = 0.0, si = 0.0;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         if (q >= nq) break;
@@ -278,9 +279,55 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
         cacc[q].x = fma(av.x, wx, fma(av.y, wy, cacc[q].x));
         cacc[q].y = fma(av.x, wy, fma(-av.y, wx, cacc[q].y));
       }
-      sr = warp_sum(sr);
-      si = warp_sum(si);
-      if (lane == 0) prow[r] = make_double2(sr, si);
+    };
+    if constexpr (NQ <= 4) {
+      // four rows per reduction: their 8 lane-partials (re, im) are summed over the warp by a
+      // transposing butterfly (9 shuffles instead of 4 x 5), and the rows' loads are not held
+      // back by a reduction after every row
+      for (int rb = j + 1 + warp; rb < n; rb += 4 * HEEV_WARPS) {
+        double v8[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = rb + u * HEEV_WARPS;
+          double sr = 0.0, si = 0.0;
+          if (r < n) row_partial(r, sr, si);
+          v8[2 * u] = sr;
+          v8[2 * u + 1] = si;
+        }
+        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+        double w4[4], w2[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double send = h16 ? v8[i] : v8[i + 4];
+          const double keep = h16 ? v8[i + 4] : v8[i];
+          w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double send = h8 ? w4[i] : w4[i + 2];
+          const double keep = h8 ? w4[i + 2] : w4[i];
+          w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        double y = (h4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? w2[0] : w2[1], 4);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        if ((lane & 3) == 0) {   // value (h16 h8 h4) = 2 u + component
+          const int idx = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+          const int r = rb + (idx >> 1) * HEEV_WARPS;
+          if (r < n) {
+            if (idx & 1) prow[r].y = y;
+            else prow[r].x = y;
+          }
+        }
+      }
+    } else {
+      for (int r = j + 1 + warp; r < n; r += HEEV_WARPS) {
+        double sr = 0.0, si = 0.0;
+        row_partial(r, sr, si);
+        sr = warp_sum(sr);
+        si = warp_sum(si);
+        if (lane == 0) prow[r] = make_double2(sr, si);
+      }
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -457,7 +504,7 @@ __device__ void tridiag_stats(const HeevProblem& P, double trace) {
 
 // ---------------------------------------------------------------- K1: tridiagonalisation
 template <int NQ>
-__global__ void __launch_bounds__(HEEV_THREADS) heev_tridiag(const HeevProblem* __restrict__ probs) {
+__global__ void __launch_bounds__(HEEV_THREADS, NQ == 4 ? 3 : 2) heev_tridiag(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
   const int n = P.n;
   cplx* A = P.A;
