@@ -280,43 +280,44 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
         cacc[q].y = fma(av.x, wy, fma(-av.y, wx, cacc[q].y));
       }
     };
-    if constexpr (NQ <= 4) {
-      // four rows per reduction: their 8 lane-partials (re, im) are summed over the warp by a
-      // transposing butterfly (9 shuffles instead of 4 x 5), and the rows' loads are not held
-      // back by a reduction after every row
-      for (int rb = j + 1 + warp; rb < n; rb += 4 * HEEV_WARPS) {
-        double v8[8];
+    if constexpr (NQ <= 6) {
+      // R rows per reduction (4 for n <= 128, 2 for n <= 192, as registers allow): their 2R
+      // lane-partials (re, im) are summed over the warp by a transposing butterfly (2R + 1
+      // shuffles instead of 5 per value), and the rows' loads are not held back by a
+      // reduction after every row
+      constexpr int R = NQ <= 4 ? 4 : 2;
+      for (int rb = j + 1 + warp; rb < n; rb += R * HEEV_WARPS) {
+        double v[2 * R];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < R; ++u) {
           const int r = rb + u * HEEV_WARPS;
           double sr = 0.0, si = 0.0;
           if (r < n) row_partial(r, sr, si);
-          v8[2 * u] = sr;
-          v8[2 * u + 1] = si;
+          v[2 * u] = sr;
+          v[2 * u + 1] = si;
         }
-        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-        double w4[4], w2[2];
+        // halve the value count per round: lanes with the round's bit set keep the upper half
+        int idx = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double send = h16 ? v8[i] : v8[i + 4];
-          const double keep = h16 ? v8[i + 4] : v8[i];
-          w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
+        for (int half = R, bit = 16; half >= 1; half >>= 1, bit >>= 1) {
+          const bool hi = lane & bit;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const double send = h8 ? w4[i] : w4[i + 2];
-          const double keep = h8 ? w4[i + 2] : w4[i];
-          w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+          for (int i = 0; i < half; ++i) {
+            const double send = hi ? v[i] : v[i + half];
+            const double keep = hi ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+          }
+          idx = 2 * idx + (hi ? 1 : 0);
         }
-        double y = (h4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? w2[0] : w2[1], 4);
-        y += __shfl_xor_sync(0xffffffffu, y, 2);
-        y += __shfl_xor_sync(0xffffffffu, y, 1);
-        if ((lane & 3) == 0) {   // value (h16 h8 h4) = 2 u + component
-          const int idx = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+        // one value left per lane; sum it over the remaining low lane bits
+        constexpr int LOWB = 32 >> (R == 4 ? 3 : 2);   // lanes sharing a value: 4 (R=4) or 8 (R=2)
+#pragma unroll
+        for (int o = LOWB >> 1; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        if ((lane & (LOWB - 1)) == 0) {   // value idx = 2 u + component
           const int r = rb + (idx >> 1) * HEEV_WARPS;
           if (r < n) {
-            if (idx & 1) prow[r].y = y;
-            else prow[r].x = y;
+            if (idx & 1) prow[r].y = v[0];
+            else prow[r].x = v[0];
           }
         }
       }
