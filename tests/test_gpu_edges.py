@@ -140,3 +140,14 @@ def test_get_data_batch_matches_per_tensor_reads(P, ctx):
         assert np.array_equal(b, ref)
     with pytest.raises(P.TTNError):
         P.ttn_get_data_batch(ctx, outs, [np.empty(sizes[0] - 1, dtype=np.complex128)] + bufs[1:])
+
+
+@pytest.mark.parametrize("chi,D,mb", [(25, 6, 32), (40, 5, 32), (33, 7, 32)])
+def test_gram_orders_between_kernel_variants(P, ctx, chi, D, mb):
+    """G-route Gram orders n = chi * D of 150, 200 and 231 at the depth-1 nodes of a 31-node
+    binary tree (m = 2 * 32 * 32 rows): between and beyond the 128 / 192 / 256 instantiations
+    of the tridiagonalisation, ragged against its row groups and its shared-memory tail;
+    truncated, GPU vs oracle."""
+    parent = W.complete_binary(31)
+    inst = W.configs.random_instance(parent, [2] * 31, chi, D, mb, seed=11)
+    run_and_check(P, ctx, inst)
