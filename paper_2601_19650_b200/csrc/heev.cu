@@ -861,6 +861,7 @@ __global__ void heev_invit(const HeevProblem* __restrict__ probs, int nprob, int
 // access instead of an L2 round trip (the global-array version K3a stalls on L2 latency).
 constexpr int INVIT_NT = 32;   // max vectors per block (fewer when 6 n NT doubles exceed the budget)
 constexpr size_t INVIT_SMEM_MAX = 200u << 10;
+constexpr size_t INVIT_SMEM_SHARED = 74u << 10;   // three blocks per SM when 8 vectors fit
 
 __global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* __restrict__ probs, int nprob,
                                                             int total, int nmax) {
@@ -1632,8 +1633,11 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::f
   {
     int mxn = 1;
     for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
+    // blocks of up to 32 vectors; the budget that keeps three blocks per SM when 8 vectors fit
+    // it (n <= 192: more vectors in flight per SM beat bigger blocks, measured), else all
+    const size_t budget = (size_t)6 * mxn * 8 * sizeof(double) <= INVIT_SMEM_SHARED ? INVIT_SMEM_SHARED : INVIT_SMEM_MAX;
     int nt = INVIT_NT;
-    while (nt > 8 && (size_t)6 * mxn * nt * sizeof(double) > INVIT_SMEM_MAX) nt /= 2;
+    while (nt > 8 && (size_t)6 * mxn * nt * sizeof(double) > budget) nt /= 2;
     const size_t ism = (size_t)6 * mxn * nt * sizeof(double);
     if (ism <= INVIT_SMEM_MAX) {
       static bool iattr = false;
