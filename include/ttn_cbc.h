@@ -64,14 +64,31 @@ typedef struct {
   int32_t host_syncs;          /* stream synchronisations taken for data-dependent ranks     */
   int32_t split_compresses;    /* partitioned apply: compresses whose Gram was row-split over
                                   ranks (partial Grams summed by allreduce); 0 otherwise      */
-  int32_t reserved;
+  int32_t exact_factors;       /* compresses taken by the exact-factor shortcut (untruncated,
+                                  certified full rank: factor = Cholesky factor of the Gram, no
+                                  eigensolver)                       */
 } ttn_cbc_report;
 
 /* ---------------------------------------------------------------- context             */
+/* Device memory source (PyTorch interop): alloc(state, bytes, stream) returns
+ * `bytes` of device memory usable in stream order on `stream` (NULL = out of memory);
+ * free(state, ptr, stream) returns it.  The library calls free only after the ctx stream
+ * has completed all work on the block, so the allocator may reuse it on any stream at once
+ * (e.g. torch.cuda.caching_allocator_alloc / caching_allocator_delete).  Callbacks may run on
+ * library worker threads (ttn_ctx_set_workers).                                          */
+typedef struct {
+  void* (*alloc)(void* state, size_t bytes, void* stream);
+  void (*free)(void* state, void* ptr, void* stream);
+  void* state;
+} ttn_allocator;
+
 /* Create a context on CUDA device `device` using stream `cuda_stream` (a cudaStream_t;
- * NULL = the legacy default stream).  Device memory comes from a cudaMallocAsync pool on
- * that stream.                                                                           */
-TTN_API ttn_status ttn_ctx_create(int device, void* cuda_stream, ttn_ctx* out);
+ * NULL = the legacy default stream).  `alloc` (may be NULL) supplies all device memory of
+ * TTN handles and of the per-apply workspaces; with NULL the context owns a stream-ordered
+ * memory pool (cudaMemPoolCreate; memory returns to the device when the ctx is destroyed).
+ * The allocator struct is copied.  Errors: ARG (bad device, NULL out, half-filled allocator),
+ * CUDA, OOM.                                                                              */
+TTN_API ttn_status ttn_ctx_create(int device, void* cuda_stream, const ttn_allocator* alloc, ttn_ctx* out);
 TTN_API ttn_status ttn_ctx_destroy(ttn_ctx ctx);
 /* Text of the last error on this ctx; valid until the next call on the ctx.             */
 TTN_API const char* ttn_last_error(ttn_ctx ctx);
@@ -138,8 +155,12 @@ TTN_API ttn_status cbc_apply(ttn_ctx ctx, ttn op, ttn state, int64_t max_bond, d
 TTN_API ttn_status cbc_apply_batch(ttn_ctx ctx, int32_t n, const ttn* ops, const ttn* states,
                            int64_t max_bond, double tol, ttn* outs, ttn_cbc_report* reps);
 
-/* <a|b>, conjugate-linear in a, by a leaves-to-root environment sweep; a and b share the
- * parent array and physical dimensions, bonds may differ.  Synchronises the stream.      */
+/* <a|b> = sum over all indices of conj(a) b, conjugate-linear in a (the inner product of
+ * Eq. 2 states; the overlap the paper's error Err = ||psi0 - U psi0|| and the
+ * fidelity checks of §IV.B rest on), by a leaves-to-root environment sweep:
+ * every node contracts conj(a_i), b_i and its children's environments into its parent-edge
+ * environment (bond_a x bond_b).  a and b share the parent array and physical dimensions,
+ * bonds may differ.  Synchronises the stream.  Errors: ARG, TOPOLOGY, SHAPE.             */
 TTN_API ttn_status ttn_overlap(ttn_ctx ctx, ttn a, ttn b, ttn_c128* out);
 /* <bra| op |ket> (one leaves-to-root sweep through bra*, op, ket); all three on one parent
  * array and physical dimensions.  With bra = cbc_apply(op, ket) this is the projection
@@ -200,7 +221,9 @@ TTN_API ttn_status ttn_profile_read(const char* family, double* ms, double* flop
 /* Number of kernels this library has launched in this process.                           */
 TTN_API ttn_status ttn_launch_count(int64_t* out);
 
-/* sqrt(Re <a|a>).                                                                         */
+/* ||a|| = sqrt(Re <a|a>) (ttn_overlap of a with itself; Eq. 2, used to normalise the
+ * initial state, reading A16, and as ||phi|| in the report).  Synchronises.
+ * Errors: ARG, TOPOLOGY.                                                                  */
 TTN_API ttn_status ttn_norm(ttn_ctx ctx, ttn a, double* out);
 
 #ifdef __cplusplus

@@ -15,7 +15,7 @@ import numpy as np
 from . import _lib as L
 from ._lib import TTN_OPERATOR, TTN_STATE, TTNError
 
-__all__ = ["Context", "TTN", "ttn_ctx_create", "ttn_create", "cbc_apply", "cbc_apply_batch", "ttn_overlap",
+__all__ = ["Context", "TTN", "torch_allocator", "ttn_ctx_create", "ttn_create", "cbc_apply", "cbc_apply_batch", "ttn_overlap",
            "ttn_overlap_batch", "ttn_norm", "ttn_get_tensor", "ttn_get_data", "ttn_get_data_batch", "ttn_version", "TTN_STATE", "TTN_OPERATOR",
            "TTNError", "lib_path"]
 
@@ -26,10 +26,31 @@ def ttn_version() -> str:
     return L.load().ttn_version().decode()
 
 
-class Context:
-    """A ttn_ctx bound to one device and one CUDA stream (default: torch's current stream)."""
+def torch_allocator(device: int):
+    """ttn_allocator over PyTorch's caching allocator (torch.cuda.caching_allocator_alloc /
+    caching_allocator_delete), so library workspaces and TTN handles share torch's memory.
+    Returns (struct, keep-alive tuple)."""
+    import torch
 
-    def __init__(self, device: int = 0, stream: Optional[int] = None):
+    def _alloc(state, nbytes, stream):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0))
+        except Exception:      # out of memory: NULL -> TTN_ERR_OOM
+            return None
+
+    def _free(state, ptr, stream):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    fa, ff = L.ALLOC_FN(_alloc), L.FREE_FN(_free)
+    return L.Allocator(fa, ff, None), (fa, ff)
+
+
+class Context:
+    """A ttn_ctx bound to one device and one CUDA stream (default: torch's current stream).
+    allocator=None: the library's own stream-ordered pool; "torch": PyTorch's caching
+    allocator (torch_allocator)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None, allocator: Optional[str] = None):
         lib = L.load()
         if stream is None:
             try:
@@ -40,8 +61,14 @@ class Context:
                 stream = None
         self.device = device
         self.stream = stream or 0
+        self._alloc = None
+        if allocator == "torch":
+            self._alloc = torch_allocator(device)
+        elif allocator is not None:
+            raise ValueError("allocator must be None or 'torch'")
         h = C.c_void_p()
-        L.check(None, lib.ttn_ctx_create(int(device), C.c_void_p(self.stream), C.byref(h)))
+        L.check(None, lib.ttn_ctx_create(int(device), C.c_void_p(self.stream),
+                                         C.byref(self._alloc[0]) if self._alloc else None, C.byref(h)))
         self.h = h
 
     def close(self):
@@ -56,20 +83,24 @@ class Context:
         self.close()
 
 
-def ttn_ctx_create(device: int = 0, stream: Optional[int] = None) -> Context:
-    return Context(device, stream)
+def ttn_ctx_create(device: int = 0, stream: Optional[int] = None, allocator: Optional[str] = None) -> Context:
+    return Context(device, stream, allocator)
 
 
 class TTN:
     """Handle of a device-resident TTNS / TTNO (immutable)."""
 
-    def __init__(self, ctx: Context, h: C.c_void_p, kind: int):
+    def __init__(self, ctx: Context, h: C.c_void_p, kind: int, src=None):
         self.ctx, self.h, self.kind = ctx, h, kind
+        # the caller's source buffers of an asynchronous (pinned / device) ttn_create: held
+        # until the handle is destroyed, so a temporary cannot be recycled before the copy ran
+        self._src = src
 
     def destroy(self):
         if self.h and self.ctx.h:      # a handle outliving its context is not freed (ctx owns the pool)
             L.load().ttn_destroy(self.h)
         self.h = None
+        self._src = None
 
     def __del__(self):
         try:
@@ -100,11 +131,33 @@ class TTN:
         return [self.get(i) for i in range(self.n_nodes)]
 
 
+def node_sizes(kind: int, parent: Sequence[int], phys: Sequence[int], bond: Sequence[int]) -> List[int]:
+    """Entries of every node tensor in the ABI leg order (include/ttn_cbc.h)."""
+    n = len(parent)
+    size = []
+    for i in range(n):
+        e = int(phys[i]) ** (2 if kind == TTN_OPERATOR else 1)
+        e *= 1 if parent[i] < 0 else int(bond[i])
+        for c in range(n):
+            if parent[c] == i:
+                e *= int(bond[c])
+        size.append(e)
+    return size
+
+
 def ttn_create(ctx: Context, kind: int, parent: Sequence[int], phys: Sequence[int], bond: Sequence[int],
                tensors: Sequence, on_device: Optional[bool] = None) -> TTN:
-    """tensors: numpy complex128 arrays (host) or torch complex128 CUDA tensors (device)."""
+    """tensors: numpy complex128 arrays (host) or torch complex128 tensors (pinned host or CUDA).
+    Each tensor's size is checked against its ABI shape before the call."""
     n = len(parent)
-    keep = []
+    if len(tensors) != n or len(phys) != n or len(bond) != n:
+        raise ValueError("one tensor, physical dimension and bond per node")
+    want = node_sizes(kind, parent, phys, bond)
+    for i, t in enumerate(tensors):
+        got = t.numel() if hasattr(t, "numel") else int(np.size(t))
+        if got != want[i]:
+            raise ValueError(f"node {i}: tensor has {got} entries, its ABI shape needs {want[i]}")
+    keep, tkeep = [], []
     ptrs = (C.c_void_p * n)()
     dev = on_device
     for i, t in enumerate(tensors):
@@ -113,7 +166,7 @@ def ttn_create(ctx: Context, kind: int, parent: Sequence[int], phys: Sequence[in
             assert t.dtype == torch.complex128 and t.is_contiguous()
             ptrs[i] = t.data_ptr()
             dev = bool(t.is_cuda) if dev is None else dev
-            keep.append(t)
+            tkeep.append(t)
         else:
             a = L.host_c128(t)
             keep.append(a)
@@ -122,7 +175,9 @@ def ttn_create(ctx: Context, kind: int, parent: Sequence[int], phys: Sequence[in
     h = C.c_void_p()
     L.check(ctx.h, L.load().ttn_create(ctx.h, int(kind), n, L.as_i32(parent), L.as_i32(phys), L.as_i64(bond),
                                        ptrs, int(bool(dev)), C.byref(h)))
-    return TTN(ctx, h, kind)
+    # pageable numpy sources are fully copied when the call returns; torch tensors (pinned
+    # host or device) are copied in stream order and stay referenced by the handle
+    return TTN(ctx, h, kind, tkeep or None)
 
 
 def ttn_get_tensor(ctx: Context, t: TTN, node: int) -> np.ndarray:

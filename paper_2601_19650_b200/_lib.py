@@ -33,10 +33,19 @@ class Report(C.Structure):
     _fields_ = [("norm", C.c_double), ("discarded_weight_sum", C.c_double), ("max_bond", C.c_int64),
                 ("peak_entries", C.c_int64), ("seconds", C.c_double), ("flops_algorithmic", C.c_double),
                 ("rank_fallbacks", C.c_int32), ("host_syncs", C.c_int32), ("split_compresses", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("exact_factors", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class Allocator(C.Structure):
+    """ttn_allocator (include/ttn_cbc.h)."""
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("state", C.c_void_p)]
 
 
 class TTNError(RuntimeError):
@@ -58,7 +67,7 @@ def load():
     lib = C.CDLL(LIB_PATH)
     P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     sig = {
-        "ttn_ctx_create": (C.c_int, [C.c_int, P, C.POINTER(P)]),
+        "ttn_ctx_create": (C.c_int, [C.c_int, P, C.POINTER(Allocator), C.POINTER(P)]),
         "ttn_ctx_destroy": (C.c_int, [P]),
         "ttn_last_error": (C.c_char_p, [P]),
         "ttn_version": (C.c_char_p, []),

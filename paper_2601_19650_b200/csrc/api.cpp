@@ -50,9 +50,15 @@ extern "C" {
 
 const char* ttn_version(void) { return "ttncbc 0.1 sm_100a (DMMA complex-FP64)"; }
 
-ttn_status ttn_ctx_create(int device, void* cuda_stream, ttn_ctx* out) {
+namespace {
+// common part of ttn_ctx_create and the worker contexts of ttn_ctx_set_workers: a worker
+// shares its parent's memory source (pool or caller allocator), so results handed to the
+// parent are freed from the source they came from
+ttn_status ctx_create_impl(int device, void* cuda_stream, const ttn_allocator* alloc, const ttn_ctx_s* parent,
+                           ttn_ctx* out) {
   if (!out) return TTN_ERR_ARG;
   *out = nullptr;
+  if (alloc && (!alloc->alloc || !alloc->free)) return TTN_ERR_ARG;
   ttn_ctx_s* c = new (std::nothrow) ttn_ctx_s();
   if (!c) return TTN_ERR_OOM;
   ttn_status s = guard(nullptr, [&] {
@@ -62,21 +68,45 @@ ttn_status ttn_ctx_create(int device, void* cuda_stream, ttn_ctx* out) {
     TTN_CUDA(cudaSetDevice(device));
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
+    if (parent) {
+      c->has_user_alloc = parent->has_user_alloc;
+      c->user_alloc = parent->user_alloc;
+      c->pool = parent->pool;
+    } else if (alloc) {
+      c->has_user_alloc = true;
+      c->user_alloc = *alloc;
+    } else {
+      // a pool of this context (the device's default pool is left as other libraries set it);
+      // freed blocks stay cached in the pool across applies, and go back to the device at
+      // ttn_ctx_destroy
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      TTN_CUDA(cudaMemPoolCreate(&c->pool, &props));
+      c->owns_pool = true;
+      uint64_t thr = UINT64_MAX;
+      TTN_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    c->scratch.set_source(c);
+    c->env.set_source(c);
     c->stager = new RingStager(c->stream);
     c->ensure_small(1 << 20);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
   });
   if (s != TTN_OK) {
     delete c->stager;
+    if (c->owns_pool) cudaMemPoolDestroy(c->pool);
     delete c;
     return s;
   }
   *out = c;
   return TTN_OK;
+}
+}  // namespace
+
+ttn_status ttn_ctx_create(int device, void* cuda_stream, const ttn_allocator* alloc, ttn_ctx* out) {
+  return ctx_create_impl(device, cuda_stream, alloc, nullptr, out);
 }
 
 ttn_status ttn_ctx_destroy(ttn_ctx ctx) {
@@ -87,10 +117,14 @@ ttn_status ttn_ctx_destroy(ttn_ctx ctx) {
   ctx->workers.clear();
   ctx->scratch.release();
   ctx->env.release();
+  cudaStreamSynchronize(ctx->stream);
+  ctx->reap(true);
   delete ctx->stager;
   delete ctx->comm;
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
   if (ctx->rank_ev) cudaEventDestroy(ctx->rank_ev);
+  // outstanding TTN handles keep their blocks: the pool is released once they are freed
+  if (ctx->owns_pool) cudaMemPoolDestroy(ctx->pool);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TTN_OK;
@@ -120,8 +154,7 @@ ttn_status ttn_create(ttn_ctx ctx, ttn_kind kind, int32_t n_nodes, const int32_t
     }
     t->bond[t->root] = 1;
     finalize_shapes(t);
-    TTN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t->data), sizeof(cplx) * std::max<int64_t>(t->total, 1),
-                             ctx->stream));
+    t->data = static_cast<cplx*>(ctx->get(sizeof(cplx) * std::max<int64_t>(t->total, 1)));
     // runs of nodes whose source tensors are adjacent in memory (a packed TTN buffer) move
     // with one copy each
     const cudaMemcpyKind kind_cp = data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -150,7 +183,7 @@ ttn_status ttn_create(ttn_ctx ctx, ttn_kind kind, int32_t n_nodes, const int32_t
   });
   if (s != TTN_OK) {
     if (t) {
-      if (t->data) cudaFreeAsync(t->data, ctx->stream);
+      if (t->data) ctx->put(t->data);
       delete t;
     }
     return s;
@@ -342,7 +375,7 @@ ttn_status ttn_ctx_set_workers(ttn_ctx ctx, int n) {
       cudaStream_t st;
       TTN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
       ttn_ctx w = nullptr;
-      ttn_status s = ttn_ctx_create(ctx->device, st, &w);
+      ttn_status s = ctx_create_impl(ctx->device, st, nullptr, ctx, &w);
       if (s != TTN_OK) {
         cudaStreamDestroy(st);
         throw Error(s, "worker context creation failed");

@@ -33,6 +33,10 @@ struct Fac {
 
 constexpr double kRankFloor = 1e-13;   // reading A4: lambda_j <= 1e-13 lambda_1 is numerically zero
 constexpr double kCholTol = 1e-13;     // relative pivot threshold of CholeskyQR (rank flag)
+// exact-factor shortcut: certified lambda_min / lambda_1 lower bound; 100x
+// above the rank floor, so the eigensolver route would keep every direction too (and so would
+// the oracle's 1e-14 sigma floor, reading A4)
+constexpr double kExactCert = 1e-11;
 
 // labels of a node contraction
 constexpr int L_SIG = 0, L_SIGP = 1, L_A = 10, L_B = 30, L_F = 50;
@@ -94,7 +98,8 @@ void check_heev_size(int64_t nn) {
 
 // Gram -> eigenpairs -> factor, for every job; synchronises once to read the ranks.
 void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_bond, double tol,
-                    ExecStats& st, std::vector<double>& w_inst, std::vector<double>& flops_inst) {
+                    ExecStats& st, std::vector<double>& w_inst, std::vector<double>& flops_inst,
+                    std::vector<int>& exact_inst) {
   if (jobs.empty()) return;
   HostScope hs_("compress_batch");
   const int nj = (int)jobs.size();
@@ -106,6 +111,17 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nj));   // pow2 range exponents
   std::vector<Pow2Problem> p2(nj);
   std::vector<int64_t> kmaxs(nj);
+  // exact-factor shortcut candidates: untruncated (tol = 0, max_bond >= min(m, n)) compresses
+  // of the tridiagonal-solver range.  W = copy of the Gram, Cholesky, L^{-1}, certificate; the
+  // eigensolver skips a certified job and its factor becomes L^H (G route) or X (K route).
+  int* d_skip = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nj));
+  int* d_cinfo = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nj));
+  TTN_CUDA(cudaMemsetAsync(d_skip, 0, sizeof(int) * nj, ctx->stream));
+  std::vector<PermProblem> ccopy;
+  std::vector<PotrfProblem> cpot;
+  std::vector<TrtriProblem> ctri;
+  std::vector<CertProblem> ccert;
+  std::vector<ExactFactorProblem> cfac;
   for (int j = 0; j < nj; ++j) {
     CompressJob& J = jobs[j];
     const int64_t m = J.m, n = J.n, nn = std::min(m, n);
@@ -153,6 +169,26 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       flops_inst[J.inst] += 8.0 * (double)kmax * n * m;
     }
     st.peak_entries = std::max(st.peak_entries, nn * nn);
+    if (tol == 0.0 && kmax == nn && !chfsi_applicable((int)nn, (int)kmax) && (m >= n || J.X)) {
+      cplx* Wc = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
+      cplx* Li = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
+      PermProblem pp{};
+      pp.src = G; pp.dst = Wc; pp.rank = 1; pp.dims[0] = nn * nn; pp.sstride[0] = 1; pp.total = nn * nn;
+      ccopy.push_back(pp);
+      cpot.push_back(PotrfProblem{Wc, nn, (int)nn, 0, d_cinfo + j, 0.0, 0.0});
+      ctri.push_back(TrtriProblem{Wc, Li, nn, (int)nn, 0});
+      ccert.push_back(CertProblem{G, Li, d_cinfo + j, d_skip + j, (int)nn, 0, kExactCert});
+      h.skip = d_skip + j;
+      ExactFactorProblem ef{};
+      ef.skip = d_skip + j;
+      if (m >= n) {
+        ef.src = Wc; ef.mode = 0; ef.rows = (int)n; ef.cols = (int)n; ef.exp2 = ej;
+      } else {
+        ef.src = J.X; ef.mode = 1; ef.rows = (int)m; ef.cols = (int)n;
+      }
+      ef.F = J.dst->p;
+      cfac.push_back(ef);
+    }
   }
   {   // the Gram squares X: exponents from the producing GEMM's epilogue where available
     std::vector<Pow2Problem> have, need, back;
@@ -166,25 +202,25 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     gemm_batch(ctx, grams, st);
     launch_pow2_restore(back.data(), (int)back.size(), *ctx->stager, ctx->stream);   // the K-route factor reads X
   }
-  static const bool dump = getenv("TTN_DEBUG_HEEV") && std::string(getenv("TTN_DEBUG_HEEV")) == "3";
-  std::vector<std::vector<cplx>> gcopy;
-  if (dump) {   // debug: keep the Grams (heev destroys them) to dump the ones that fail
-    cudaStreamSynchronize(ctx->stream);
-    for (auto& h : hp) {
-      gcopy.emplace_back((size_t)h.n * h.n);
-      cudaMemcpy(gcopy.back().data(), h.A, sizeof(cplx) * h.n * h.n, cudaMemcpyDeviceToHost);
-    }
+  if (!ccert.empty()) {   // exact-factor shortcut: Cholesky of a copy of each candidate's Gram
+    launch_permute(ccopy.data(), (int)ccopy.size(), *ctx->stager, ctx->stream);
+    launch_potrf(cpot.data(), (int)cpot.size(), *ctx->stager, ctx->stream);
+    launch_trtri(ctri.data(), (int)ctri.size(), *ctx->stager, ctx->stream);
+    launch_chol_certify(ccert.data(), (int)ccert.size(), *ctx->stager, ctx->stream);
   }
-  static const bool dbg = getenv("TTN_DEBUG_HEEV") != nullptr;
   // ranks and discarded weights go to the host as soon as the eigenvalue stages have fixed them:
   // the host waits on that point only, and builds the next level while the eigenvector stages
   // and the factor kernels still run (the next level's launches queue behind them)
-  ctx->ensure_small(sizeof(int) * nj + sizeof(double) * nj);
+  // pinned layout: ranks (padded to 8 bytes), discarded weights, shortcut flags
+  const size_t small_bytes = sizeof(int) * ((nj + 1) & ~1) + sizeof(double) * nj + sizeof(int) * nj;
+  ctx->ensure_small(small_bytes);
   int* hk = reinterpret_cast<int*>(ctx->hbuf);
   double* hw = reinterpret_cast<double*>(ctx->hbuf + sizeof(int) * ((nj + 1) & ~1));
+  int* hs = reinterpret_cast<int*>(hw + nj);
   auto read_ranks = [&]() {
     TTN_CUDA(cudaMemcpyAsync(hk, d_k, sizeof(int) * nj, cudaMemcpyDeviceToHost, ctx->stream));
     TTN_CUDA(cudaMemcpyAsync(hw, d_w, sizeof(double) * nj, cudaMemcpyDeviceToHost, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(hs, d_skip, sizeof(int) * nj, cudaMemcpyDeviceToHost, ctx->stream));
   };
   bool early = false;
   {   // small Grams: tridiagonal pipeline (heev.cu); large ones: Chebyshev subspace (chfsi.cu)
@@ -195,7 +231,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       else small.push_back(h);
     }
     std::function<void()> ready;
-    if (large.empty() && !dbg)
+    if (large.empty())
       ready = [&]() {
         read_ranks();
         ctx->mark_ranks();
@@ -206,50 +242,24 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   }
   if (!sr.empty()) launch_scale_rows(sr.data(), (int)sr.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, fgemm, st);
+  launch_exact_factor(cfac.data(), (int)cfac.size(), *ctx->stager, ctx->stream);   // certified jobs
   if (early) {
     ctx->wait_ranks();
   } else {
     // the Chebyshev solver may have grown (reallocated) the small pinned buffer: re-derive
-    ctx->ensure_small(sizeof(int) * nj + sizeof(double) * nj);
+    ctx->ensure_small(small_bytes);
     hk = reinterpret_cast<int*>(ctx->hbuf);
     hw = reinterpret_cast<double*>(ctx->hbuf + sizeof(int) * ((nj + 1) & ~1));
+    hs = reinterpret_cast<int*>(hw + nj);
     read_ranks();
     ctx->sync();
-  }
-  if (dbg) {   // debug: every eigenvector block and factor must be finite
-    for (int j = 0; j < nj; ++j) {
-      const HeevProblem& h = hp[j];
-      std::vector<cplx> vt((size_t)h.kmax * h.n), f((size_t)h.kmax * jobs[j].n);
-      std::vector<double> lam(h.kmax);
-      cudaMemcpy(vt.data(), h.Vt, sizeof(cplx) * vt.size(), cudaMemcpyDeviceToHost);
-      cudaMemcpy(f.data(), jobs[j].dst->p, sizeof(cplx) * f.size(), cudaMemcpyDeviceToHost);
-      cudaMemcpy(lam.data(), h.lam, sizeof(double) * lam.size(), cudaMemcpyDeviceToHost);
-      bool ok = true;
-      for (auto& v : vt) ok = ok && std::isfinite(v.x) && std::isfinite(v.y);
-      bool okf = true;
-      for (auto& v : f) okf = okf && std::isfinite(v.x) && std::isfinite(v.y);
-      std::vector<cplx> xx((size_t)jobs[j].m * jobs[j].n);
-      cudaMemcpy(xx.data(), jobs[j].X, sizeof(cplx) * xx.size(), cudaMemcpyDeviceToHost);
-      bool okx = true;
-      for (auto& v : xx) okx = okx && std::isfinite(v.x) && std::isfinite(v.y);
-      static const bool all = std::string(getenv("TTN_DEBUG_HEEV")) == "2";
-      if (dump && !ok) {
-        char fn[256];
-        snprintf(fn, sizeof(fn), "gpurun_out/bad_gram_%d_n%d_k%d.bin", j, h.n, h.kmax);
-        FILE* fp = fopen(fn, "wb");
-        if (fp) { fwrite(gcopy[j].data(), sizeof(cplx), gcopy[j].size(), fp); fclose(fp); }
-      }
-      if (!ok || !okf || !okx || all)
-        fprintf(stderr, "[heev] job %d F=%p m=%lld n=%lld nn=%d kmax=%d k=%d w=%g lam0=%g lamk=%g Vt_finite=%d F_finite=%d X_finite=%d\n", j,
-                (void*)jobs[j].dst->p, (long long)jobs[j].m, (long long)jobs[j].n, h.n, h.kmax, hk[j], hw[j], lam[0],
-                lam[h.kmax - 1], ok, okf, okx);
-    }
   }
   for (int j = 0; j < nj; ++j) {
     if (hk[j] < 1 || hk[j] > kmaxs[j]) throw Error(TTN_ERR_NUMERIC, "eigensolver returned an invalid rank");
     if (!std::isfinite(hw[j])) throw Error(TTN_ERR_NUMERIC, "non-finite discarded weight (non-finite input?)");
     jobs[j].dst->k = hk[j];
     w_inst[jobs[j].inst] += hw[j];
+    exact_inst[jobs[j].inst] += hs[j] ? 1 : 0;
   }
 }
 
@@ -446,7 +456,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   // per-instance accumulators: replicated top work counted on every rank, subtree work only
   // on its owner (summed over ranks at the end)
   std::vector<double> w_inst(nb, 0.0), flops_inst(nb, 0.0), w_sub(nb, 0.0), flops_sub(nb, 0.0);
-  std::vector<int> fb_inst(nb, 0), fb_sub(nb, 0), split_inst(nb, 0);
+  std::vector<int> fb_inst(nb, 0), fb_sub(nb, 0), split_inst(nb, 0), exact_inst(nb, 0), exact_sub(nb, 0);
   std::vector<Fac> up((size_t)nb * n), down((size_t)nb * n), R((size_t)nb * n);
   // trivial factor L^{[(-,r)]} = 1 (extent-1 legs)
   cplx* one = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx)));
@@ -455,6 +465,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
 
   auto acc_w = [&](bool sub) -> std::vector<double>& { return sub ? w_sub : w_inst; };
   auto acc_f = [&](bool sub) -> std::vector<double>& { return sub ? flops_sub : flops_inst; };
+  auto acc_x = [&](bool sub) -> std::vector<int>& { return sub ? exact_sub : exact_inst; };
 
   // ---------------- row split of the replicated top's heavy compresses (partitioned apply):
   // a G-route compress of X (rows m >= cols n) whose widest factor leg has extent k is cut into
@@ -554,7 +565,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       sp_j[q].exp = d_e + q;
       sp_j[q].X = nullptr;
     }
-    compress_batch(ctx, sp_j, max_bond, tol, st, w_inst, flops_inst);
+    compress_batch(ctx, sp_j, max_bond, tol, st, w_inst, flops_inst, exact_inst);
   };
 
   // ---------------- 1. up-sweep (Eq. 10) over the nodes selected by `sel`, deepest level first
@@ -593,7 +604,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
       for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst] += tasks[j].flops;
       st.flops += cs.flops;
-      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub));
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub));
       ctx->scratch.reset();
     }
   };
@@ -637,7 +648,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
       for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst] += tasks[j].flops;
       st.flops += cs.flops;
-      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub));
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub));
       ctx->scratch.reset();
     }
   };
@@ -798,7 +809,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
 
   // ---------------- report: ||phi|| = ||T'_root||_F; subtree totals summed over ranks
   std::vector<SumsqProblem> sq(nb);
-  double* d_sq = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nb * 4));
+  double* d_sq = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nb * 5));
   for (int b = 0; b < nb; ++b) {
     sq[b].x = outs[b]->node(root);
     sq[b].len = 1;
@@ -807,20 +818,22 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   }
   launch_sumsq(sq.data(), nb, *ctx->stager, ctx->stream);
   if (part.on) {
-    std::vector<double> h(3 * (size_t)nb);
+    std::vector<double> h(4 * (size_t)nb);
     for (int b = 0; b < nb; ++b) {
       h[b] = w_sub[b];
       h[nb + b] = flops_sub[b];
       h[2 * nb + b] = fb_sub[b];
+      h[3 * nb + b] = exact_sub[b];
     }
-    TTN_CUDA(cudaMemcpyAsync(d_sq + nb, h.data(), sizeof(double) * 3 * nb, cudaMemcpyHostToDevice, ctx->stream));
-    comm->allreduce_sum(d_sq + nb, 3 * (size_t)nb, ctx->stream);
-    TTN_CUDA(cudaMemcpyAsync(h.data(), d_sq + nb, sizeof(double) * 3 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(d_sq + nb, h.data(), sizeof(double) * 4 * nb, cudaMemcpyHostToDevice, ctx->stream));
+    comm->allreduce_sum(d_sq + nb, 4 * (size_t)nb, ctx->stream);
+    TTN_CUDA(cudaMemcpyAsync(h.data(), d_sq + nb, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
     for (int b = 0; b < nb; ++b) {
       w_inst[b] += h[b];
       flops_inst[b] += h[nb + b];
       fb_inst[b] += (int)std::lround(h[2 * nb + b]);
+      exact_inst[b] += (int)std::lround(h[3 * nb + b]);
     }
   }
   ctx->ensure_small(sizeof(double) * nb);
@@ -853,7 +866,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       r.rank_fallbacks = fb_inst[b];
       r.host_syncs = ctx->host_syncs;
       r.split_compresses = split_inst[b];
-      r.reserved = 0;
+      r.exact_factors = exact_inst[b];
     }
   }
 }

@@ -474,7 +474,80 @@ __global__ void __launch_bounds__(256) geqr_q_grouped(const GeqrProblem* __restr
   }
 }
 
+// one CTA per Gram: ||Li||_F^2 over the lower triangle and tr W, then the certificate
+__global__ void __launch_bounds__(256) chol_certify(const CertProblem* __restrict__ probs) {
+  const CertProblem P = probs[blockIdx.x];
+  __shared__ double red[32];
+  const int n = P.n;
+  double s = 0.0, tr = 0.0;
+  for (long long g = threadIdx.x; g < (long long)n * n; g += blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    if (j <= i) {
+      const cplx v = P.Li[g];
+      s += v.x * v.x + v.y * v.y;
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tr += P.W[(size_t)i * n + i].x;
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = s;
+    red[16 + (threadIdx.x >> 5)] = tr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double S = 0.0, T = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      S += red[w];
+      T += red[16 + w];
+    }
+    const bool ok = *P.info == 0 && S > 0.0 && T > 0.0 && isfinite(S) && isfinite(T) && 1.0 / (S * T) >= P.thresh;
+    *P.skip = ok ? 1 : 0;
+  }
+}
+
+__global__ void exact_factor(const ExactFactorProblem* __restrict__ probs) {
+  const ExactFactorProblem P = probs[blockIdx.y];
+  if (!*P.skip) return;
+  const double sc = (P.mode == 0 && P.exp2) ? ldexp(1.0, pow2_effective(*P.exp2)) : 1.0;
+  const long long tot = (long long)P.rows * P.cols;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < tot; g += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(g / P.cols), c = (int)(g % P.cols);
+    cplx v;
+    if (P.mode == 0) {
+      v = c >= t ? P.src[(size_t)c * P.cols + t] : make_double2(0.0, 0.0);
+      v.x *= sc;
+      v.y *= -sc;   // F = 2^e L^H
+    } else {
+      v = P.src[g];
+    }
+    P.F[g] = v;
+  }
+}
+
 }  // namespace
+
+void launch_chol_certify(CertProblem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  const CertProblem* d = static_cast<const CertProblem*>(st.put(h, sizeof(CertProblem) * n));
+  prof_begin(s);
+  chol_certify<<<n, 256, 0, s>>>(d);
+  prof_end(s, "potrf", 0.0, 0.0);
+  count_launch();
+}
+
+void launch_exact_factor(ExactFactorProblem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  long long mx = 1;
+  for (int i = 0; i < n; ++i) mx = std::max<long long>(mx, (long long)h[i].rows * h[i].cols);
+  const ExactFactorProblem* d = static_cast<const ExactFactorProblem*>(st.put(h, sizeof(ExactFactorProblem) * n));
+  prof_begin(s);
+  exact_factor<<<dim3((unsigned)std::min<long long>((mx + 255) / 256, 64), n), 256, 0, s>>>(d);
+  prof_end(s, "misc", 0.0, 32.0 * (double)mx * n);
+  count_launch();
+}
 
 void launch_geqr_q(GeqrProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
@@ -495,20 +568,11 @@ void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s) {
   int mx = 1;
   for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].n);
   const size_t smem = (size_t)mx * CH_NB * sizeof(cplx);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(potrf_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 << 10));
-    attr = smem;
-  }
+  if (mx > CH_SMALL) func_smem(potrf_grouped, std::max<size_t>(smem, 48 << 10));
   prof_begin(s);
   if (mx <= CH_SMALL) {
     const size_t sm = (size_t)mx * (mx + 1) * sizeof(cplx);
-    static bool sattr = false;
-    if (!sattr) {
-      cudaFuncSetAttribute(potrf_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((size_t)CH_SMALL * (CH_SMALL + 1) * sizeof(cplx)));
-      sattr = true;
-    }
+    func_smem(potrf_small, (size_t)CH_SMALL * (CH_SMALL + 1) * sizeof(cplx));
     potrf_small<<<n, 256, sm, s>>>(d);
   } else {
     potrf_grouped<<<n, CH_THREADS, smem, s>>>(d);
@@ -525,20 +589,11 @@ void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s) {
   int mx = 1;
   for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].n);
   const size_t smem = (size_t)mx * CH_NB * sizeof(cplx);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(trtri_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 << 10));
-    attr = smem;
-  }
+  if (mx > CH_SMALL) func_smem(trtri_grouped, std::max<size_t>(smem, 48 << 10));
   prof_begin(s);
   if (mx <= CH_SMALL) {
     const size_t sm = (2 * (size_t)mx * (mx + 1) + mx) * sizeof(cplx);
-    static bool sattr = false;
-    if (!sattr) {
-      cudaFuncSetAttribute(trtri_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((2 * (size_t)CH_SMALL * (CH_SMALL + 1) + CH_SMALL) * sizeof(cplx)));
-      sattr = true;
-    }
+    func_smem(trtri_small, (2 * (size_t)CH_SMALL * (CH_SMALL + 1) + CH_SMALL) * sizeof(cplx));
     trtri_small<<<n, 4 * CH_SMALL, sm, s>>>(d);
   } else {
     trtri_grouped<<<n, CH_THREADS, smem, s>>>(d);

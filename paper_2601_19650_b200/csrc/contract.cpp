@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <unordered_map>
@@ -274,21 +275,29 @@ void plan_key(const Task& t, std::vector<int64_t>& k) {
   for (int l : t.out_labels) k.push_back(l);
 }
 
+// Plans are shared: a batch (and other worker threads) keep the plans they use alive while
+// the cache evicts, so bounding the cache never frees a plan in use.
+using PlanPtr = std::shared_ptr<const PlanT>;
 std::mutex g_plan_mu;
-std::unordered_map<std::vector<int64_t>, PlanT, KeyHash>& plan_cache() {
-  static std::unordered_map<std::vector<int64_t>, PlanT, KeyHash> c;
+std::unordered_map<std::vector<int64_t>, PlanPtr, KeyHash>& plan_cache() {
+  static std::unordered_map<std::vector<int64_t>, PlanPtr, KeyHash> c;
   return c;
 }
 
-const PlanT& get_plan(const Task& t) {
+PlanPtr get_plan(const Task& t) {
   thread_local std::vector<int64_t> key;
   plan_key(t, key);
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto& c = plan_cache();
+    auto it = c.find(key);
+    if (it != c.end()) return it->second;
+  }
+  PlanPtr p = std::make_shared<const PlanT>(make_plan(t));   // planned outside the lock
   std::lock_guard<std::mutex> lk(g_plan_mu);
   auto& c = plan_cache();
-  auto it = c.find(key);
-  if (it != c.end()) return it->second;
-  if (c.size() > 200000) c.clear();
-  return c.emplace(key, make_plan(t)).first->second;
+  if (c.size() > 200000) c.clear();   // in-use plans survive through their shared owners
+  return c.emplace(key, p).first->second;
 }
 
 }  // namespace
@@ -351,30 +360,12 @@ GemmProblem mk_gemm(const cplx* A, int opA, long long lda, const cplx* B, int op
 void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st) {
   HostScope hs_("contract_batch");
   if (tasks.empty()) return;
-  static const bool dbg0 = getenv("TTN_DEBUG_CONTRACT") != nullptr;
-  if (dbg0) {   // debug: inputs must be finite before any launch of this batch
-    cudaStreamSynchronize(ctx->stream);
-    for (size_t i = 0; i < tasks.size(); ++i)
-      for (size_t j = 0; j < tasks[i].ops.size(); ++j) {
-        const Operand& o = tasks[i].ops[j];
-        int64_t e = 1;
-        for (auto d : o.dims) e *= d;
-        std::vector<cplx> h((size_t)e);
-        cudaMemcpy(h.data(), o.ptr, sizeof(cplx) * e, cudaMemcpyDeviceToHost);
-        for (auto& v : h)
-          if (!std::isfinite(v.x) || !std::isfinite(v.y)) {
-            fprintf(stderr, "[contract] BEFORE launch: task %zu operand %zu non-finite (ptr %p, %lld elems)\n", i, j,
-                    (const void*)o.ptr, (long long)e);
-            break;
-          }
-      }
-  }
-  std::vector<const PlanT*> plans(tasks.size());
+  std::vector<PlanPtr> plans(tasks.size());
   size_t max_steps = 0;
   std::vector<PermProblem> perms;
   for (size_t i = 0; i < tasks.size(); ++i) {
     Task& t = tasks[i];
-    plans[i] = &get_plan(t);
+    plans[i] = get_plan(t);
     t.out_dims.clear();
     int64_t tot = 1;
     for (int l : t.out_labels) {   // extent of each output label (first operand carrying it)
@@ -435,52 +426,6 @@ void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st) {
       round.push_back(g);
     }
     gemm_batch(ctx, round, st);
-  }
-  static const bool dbg = getenv("TTN_DEBUG_CONTRACT") != nullptr;
-  if (dbg) {   // debug: report the first task whose output is non-finite while its inputs are finite
-    cudaStreamSynchronize(ctx->stream);
-    auto finite = [](const cplx* p, int64_t n) {
-      std::vector<cplx> h((size_t)n);
-      cudaMemcpy(h.data(), p, sizeof(cplx) * n, cudaMemcpyDeviceToHost);
-      for (auto& v : h)
-        if (!std::isfinite(v.x) || !std::isfinite(v.y)) return false;
-      return true;
-    };
-    for (size_t i = 0; i < tasks.size(); ++i) {
-      Task& t = tasks[i];
-      int64_t tot = 1;
-      for (auto d : t.out_dims) tot *= d;
-      if (finite(t.out, tot)) continue;
-      bool in_ok = true;
-      std::string fl;
-      for (auto& o : t.ops) {
-        int64_t e = 1;
-        for (auto d : o.dims) e *= d;
-        const bool f = finite(o.ptr, e);
-        fl += f ? "1" : "0";
-        in_ok = in_ok && f;
-      }
-      fprintf(stderr, "[contract] task %zu non-finite output, inputs finite=%s; ops:", i, fl.c_str());
-      for (auto& o : t.ops) {
-        fprintf(stderr, " [");
-        for (size_t j = 0; j < o.labels.size(); ++j) fprintf(stderr, "%d:%lld ", o.labels[j], (long long)o.dims[j]);
-        fprintf(stderr, "]");
-      }
-      fprintf(stderr, " -> [");
-      for (int l : t.out_labels) fprintf(stderr, "%d ", l);
-      fprintf(stderr, "]\n");
-      for (auto& s : plans[i]->steps) {
-        const GemmProblem& g = s.g;
-        fprintf(stderr, "   step a=%d b=%d M=%d N=%d K=%d legs %d/%d/%d md=", s.a, s.b, g.M, g.N, g.K, g.nm, g.nn, g.nk);
-        for (int q = 0; q < g.nm; ++q) fprintf(stderr, "%d(am%lld,cm%lld) ", g.md[q], g.am[q], g.cm[q]);
-        fprintf(stderr, " nd=");
-        for (int q = 0; q < g.nn; ++q) fprintf(stderr, "%d(bn%lld,cn%lld) ", g.nd[q], g.bn[q], g.cn[q]);
-        fprintf(stderr, " kd=");
-        for (int q = 0; q < g.nk; ++q) fprintf(stderr, "%d(ak%lld,bk%lld) ", g.kd[q], g.ak[q], g.bk[q]);
-        fprintf(stderr, "\n");
-      }
-      if (in_ok) break;
-    }
   }
 }
 

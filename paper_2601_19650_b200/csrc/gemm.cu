@@ -511,12 +511,7 @@ void launch_variant(const GemmProblem* d, int n, int tiles, cudaStream_t s) {
   constexpr int ST = Occ<BM, BN>::ST, MINB = Occ<BM, BN>::MINB;
   using C_ = Cfg<BM, BN, AKM, BNM, ST>;
   static_assert(MINB * C_::BYTES <= 227 * 1024, "shared memory for the resident CTAs");
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, C_::BYTES);
-    attr_done = true;
-  }
+  func_smem(zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB>, C_::BYTES);
   const int grid = std::min(tiles, MINB * 148);   // persistent: MINB resident CTAs per SM
   zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB><<<grid, THREADS, C_::BYTES, s>>>(d, n, tiles);
   count_launch();

@@ -507,6 +507,7 @@ __device__ void tridiag_stats(const HeevProblem& P, double trace) {
 template <int NQ>
 __global__ void __launch_bounds__(HEEV_THREADS, NQ == 4 ? 3 : 2) heev_tridiag(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
+  if (P.skip && *P.skip) return;   // exact-factor shortcut (chol_certify)
   const int n = P.n;
   cplx* A = P.A;
   const int tid = threadIdx.x;
@@ -552,6 +553,7 @@ __global__ void __launch_bounds__(CL_THREADS) heev_tridiag_cluster(const HeevPro
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const HeevProblem P = probs[blockIdx.x / CS];
+  if (P.skip && *P.skip) return;   // uniform over the cluster
   const int n = P.n, rpc = (n + CS - 1) / CS, r0 = rank * rpc, r1 = min(n, r0 + rpc);
   cplx* A = P.A;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -711,9 +713,10 @@ __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, in
   const double* d = P.work;
   const double* e = P.work + n;
   const double* sc = P.work + 2 * n;
-  const double pivmin = sc[S_PIVMIN], atol = sc[S_ATOL];
+  const bool skipped = P.skip && *P.skip;       // still takes part in the warp's ballots
+  const double pivmin = skipped ? 0.0 : sc[S_PIVMIN], atol = skipped ? 1.0 : sc[S_ATOL];
   const int idx = n - 1 - t;                   // ascending index of the t-th largest
-  double lo = sc[S_GL], hi = sc[S_GU];
+  double lo = skipped ? 0.0 : sc[S_GL], hi = skipped ? 0.0 : sc[S_GU];
   for (int it = 0; it < 96; ++it) {
     const bool done = hi - lo <= fmax(atol, 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) + pivmin;
     if (__all_sync(0xffffffffu, done)) break;
@@ -744,7 +747,7 @@ __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, in
       hi = nhi;
     }
   }
-  if (sub == 0 && g0 < total) P.lam[t] = 0.5 * (lo + hi);
+  if (sub == 0 && g0 < total && !skipped) P.lam[t] = 0.5 * (lo + hi);
 }
 
 // ---------------------------------------------------------------- K3: inverse iteration
@@ -752,6 +755,7 @@ __global__ void heev_invit(const HeevProblem* __restrict__ probs, int nprob, int
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= total) return;
   const HeevProblem& P = probs[find_estart(probs, nprob, g)];
+  if (P.skip && *P.skip) return;
   const int t = g - P.estart, n = P.n, kmax = P.kmax;
   const double* __restrict__ sd = P.work;
   const double* __restrict__ evec = P.work + n;
@@ -871,6 +875,7 @@ __global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* _
   const int g = blockIdx.x * NT + tl;
   if (g >= total) return;
   const HeevProblem& P = probs[find_estart(probs, nprob, g)];
+  if (P.skip && *P.skip) return;
   const int t = g - P.estart, n = P.n, kmax = P.kmax;
   const double* __restrict__ sd = P.work;
   const double* __restrict__ evec = P.work + n;
@@ -972,6 +977,7 @@ __global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* _
 // ---------------------------------------------------------------- K4: CholeskyQR2 of Z
 __global__ void __launch_bounds__(HEEV_THREADS) heev_orth(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
+  if (P.skip && *P.skip) return;
   const int n = P.n, kmax = P.kmax, tid = threadIdx.x;
   const int k = P.k_out ? *P.k_out : kmax;   // only the kept directions are orthonormalised
   {   // isolated eigenvalues (gap > 1e-5 ||T||): inverse-iteration vectors are already orthogonal
@@ -1029,6 +1035,7 @@ __host__ __device__ inline size_t orth_smem_bytes(int kmax) {
 
 __global__ void __launch_bounds__(HEEV_THREADS) heev_orth_smem(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
+  if (P.skip && *P.skip) return;
   const int n = P.n, kmax = P.kmax, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = P.k_out ? *P.k_out : kmax;
   {
@@ -1174,6 +1181,7 @@ __global__ void heev_backtr(const HeevProblem* __restrict__ probs, int nprob, in
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= total) return;
   const HeevProblem& P = probs[find_estart(probs, nprob, gw)];
+  if (P.skip && *P.skip) return;
   const int t = gw - P.estart, n = P.n, kmax = P.kmax;
   const double* Z = P.work + 2 * n + 8;
   const cplx* A = P.A;
@@ -1215,7 +1223,7 @@ __global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob, i
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nprob) return;
   const HeevProblem& P = probs[i];
-  if (!P.exp2) return;
+  if (!P.exp2 || (P.skip && *P.skip)) return;
   const int e = pow2_effective(*P.exp2);
   if (e == 0) return;
   if (what & 2)
@@ -1247,6 +1255,7 @@ __global__ void __launch_bounds__(BT_WARPS * 32) heev_backtr_blk(const HeevProbl
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const HeevProblem& P = probs[find_bstart(probs, nprob, blockIdx.x)];
+  if (P.skip && *P.skip) return;
   const int t0 = (blockIdx.x - P.bstart) * BT_WARPS * VPW, tw = t0 + warp * VPW, n = P.n, kmax = P.kmax;
   cplx* sv = reinterpret_cast<cplx*>(smem_raw);
   cplx* stau = sv + (size_t)BT_R * n;
@@ -1337,6 +1346,11 @@ __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
   if (i >= nprob) return;
   const HeevProblem& P = probs[i];
   const int kmax = P.kmax;
+  if (P.skip && *P.skip) {   // exact-factor shortcut: every direction kept, nothing discarded
+    if (P.k_out) *P.k_out = kmax;
+    if (P.w_out) *P.w_out = 0.0;
+    return;
+  }
   const double trace = P.work[2 * P.n + S_TRACE];
   const double l1 = P.lam[0];
   int k = 1;
@@ -1386,6 +1400,7 @@ __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
 // after another.
 __global__ void __launch_bounds__(HEEV_THREADS) heev_invit_cluster(const HeevProblem* __restrict__ probs) {
   const HeevProblem P = probs[blockIdx.x];
+  if (P.skip && *P.skip) return;
   const int n = P.n, kmax = P.kmax, tid = threadIdx.x;
   const int k = P.k_out ? *P.k_out : kmax;
   const double* sd = P.work;
@@ -1523,12 +1538,9 @@ int heev_max_n() { return HEEV_MAX_N; }
 namespace {
 template <int CS>
 void launch_cl(const HeevProblem* d, int nprob, size_t smem, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(heev_tridiag_cluster<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CL_SMEM_LIMIT);
-    if (CS > 8) cudaFuncSetAttribute(heev_tridiag_cluster<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
-  }
+  func_smem(heev_tridiag_cluster<CS>, CL_SMEM_LIMIT);
+  if (CS > 8)
+    func_attr(reinterpret_cast<const void*>(heev_tridiag_cluster<CS>), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nprob * CS);
   cfg.blockDim = dim3(CL_THREADS);
@@ -1556,13 +1568,9 @@ void launch_tridiag_cluster(const HeevProblem* d, int nprob, int cs, size_t smem
 void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::function<void()>& values_ready) {
   HostScope hs_("launch_heev");
   if (n == 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(heev_tridiag<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
-    cudaFuncSetAttribute(heev_tridiag<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
-    cudaFuncSetAttribute(heev_tridiag<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM_BUDGET);
-    attr = true;
-  }
+  func_smem(heev_tridiag<4>, FUSED_SMEM_BUDGET);
+  func_smem(heev_tridiag<6>, FUSED_SMEM_BUDGET);
+  func_smem(heev_tridiag<8>, FUSED_SMEM_BUDGET);
   int total = 0;
   double fl = 0.0, by = 0.0;
   int nblk = 0;
@@ -1640,11 +1648,7 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::f
     while (nt > 8 && (size_t)6 * mxn * nt * sizeof(double) > budget) nt /= 2;
     const size_t ism = (size_t)6 * mxn * nt * sizeof(double);
     if (ism <= INVIT_SMEM_MAX) {
-      static bool iattr = false;
-      if (!iattr) {
-        cudaFuncSetAttribute(heev_invit_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)INVIT_SMEM_MAX);
-        iattr = true;
-      }
+      func_smem(heev_invit_smem, INVIT_SMEM_MAX);
       heev_invit_smem<<<(total + nt - 1) / nt, nt, ism, s>>>(d, n, total, mxn);
     } else {
       heev_invit<<<(total + 127) / 128, 128, 0, s>>>(d, n, total);
@@ -1656,11 +1660,7 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::f
     int mk = 0;
     for (int i = 0; i < n; ++i) mk = std::max(mk, h[i].kmax);
     if (mk <= ORTH_SMEM_K) {
-      static bool oattr = false;
-      if (!oattr) {
-        cudaFuncSetAttribute(heev_orth_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)orth_smem_bytes(ORTH_SMEM_K));
-        oattr = true;
-      }
+      func_smem(heev_orth_smem, orth_smem_bytes(ORTH_SMEM_K));
       heev_orth_smem<<<n, HEEV_THREADS, orth_smem_bytes(mk), s>>>(d);
     } else {
       heev_orth<<<n, HEEV_THREADS, 0, s>>>(d);
@@ -1670,13 +1670,9 @@ void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::f
     int mxn = 0;
     for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
     if (mxn <= 256) {
-      static bool battr = false;
-      if (!battr) {
-        cudaFuncSetAttribute(heev_backtr_blk<4, BT_VPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
-        cudaFuncSetAttribute(heev_backtr_blk<6, BT_VPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
-        cudaFuncSetAttribute(heev_backtr_blk<8, BT_VPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backtr_smem_bytes(256));
-        battr = true;
-      }
+      func_smem(heev_backtr_blk<4, BT_VPW>, backtr_smem_bytes(256));
+      func_smem(heev_backtr_blk<6, BT_VPW>, backtr_smem_bytes(256));
+      func_smem(heev_backtr_blk<8, BT_VPW>, backtr_smem_bytes(256));
       if (mxn <= 128) heev_backtr_blk<4, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
       else if (mxn <= 192) heev_backtr_blk<6, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
       else heev_backtr_blk<8, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);

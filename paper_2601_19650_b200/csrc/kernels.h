@@ -84,6 +84,9 @@ struct HeevProblem {
   int bstart;          // filled by the launcher: first back-transform block of this problem
   const int* exp2;     // may be null: A was formed from data scaled by 2^-e (pow2_normalize);
                        // the returned eigenvalues and discarded weight are scaled by 2^(2e)
+  const int* skip;     // may be null: *skip != 0 (set on the device by chol_certify) = the
+                       // exact-factor shortcut took this compress: every stage skips it, and
+                       // k = kmax, w = 0 are written (lam / Vt are left unset)
 };
 size_t heev_work_doubles(int n, int kmax);
 size_t heev_smem_bytes(int n, int kmax);
@@ -108,6 +111,33 @@ struct TrtriProblem {
   cplx* Linv;
   long long ld;
   int n;
+  int pad_;
+};
+
+// Exact-factor shortcut of an untruncated compress ("G = M^dagger M,
+// which is a Cholesky decomposition of G"): with L L^H = W (potrf of a copy of the Gram W) and
+// Li = L^{-1} (trtri), lambda_min(W) >= 1 / ||Li||_F^2 and lambda_1(W) <= tr W, so
+// 1 / (||Li||_F^2 tr W) >= thresh certifies that every eigenvalue passes the rank floor and
+// the eigensolver would keep all of them.  *skip = (info == 0 && certified).
+struct CertProblem {
+  const cplx* W;       // the Gram (n x n, ld n; its diagonal is read)
+  const cplx* Li;      // L^{-1} (n x n lower, ld n)
+  const int* info;     // potrf status of the copy
+  int* skip;
+  int n;
+  int pad_;
+  double thresh;
+};
+// Factor of a certified compress, written over the eigensolver route's output when *skip:
+//   mode 0 (G route, W = X^H X = L L^H):  F = L^H  (n x n upper; F^H F = W exactly);
+//   mode 1 (K route, m <= max_bond):      F = X    (m x n; F^H F = X^H X trivially).
+struct ExactFactorProblem {
+  const cplx* src;     // mode 0: L (n x n lower, ld cols); mode 1: X (rows x cols)
+  cplx* F;             // rows x cols
+  const int* skip;
+  const int* exp2;     // mode 0, may be null: W was formed from X scaled by 2^-e, F is scaled by 2^e
+  int rows, cols;
+  int mode;
   int pad_;
 };
 
@@ -147,6 +177,8 @@ void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s,
                  const std::function<void()>& values_ready = std::function<void()>());
 void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_chol_certify(CertProblem* h, int n, Stager& st, cudaStream_t s);
+void launch_exact_factor(ExactFactorProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_scale_rows(ScaleRowsProblem* h, int n, Stager& st, cudaStream_t s);
 // out[j] = sum_i |x_j[i]|^2 of n device vectors
@@ -173,6 +205,15 @@ void launch_pow2_apply(Pow2Problem* h, int n, Stager& st, cudaStream_t s);
 // *exp = "no data yet" for n contiguous exponents
 void pow2_reset(int* exp, int n, cudaStream_t s);
 __host__ __device__ inline int pow2_effective(int e) { return (e < -2000 || (e > -100 && e < 100)) ? 0 : e; }
+
+// cudaFuncSetAttribute on the CURRENT device, once per (device, function, attribute) and only
+// ever raising the value (thread-safe): a kernel attribute is per device, and contexts on
+// several devices or worker threads may launch the same kernel.
+void func_attr(const void* func, cudaFuncAttribute attr, int value);
+template <typename F>
+inline void func_smem(F* func, size_t bytes) {
+  func_attr(reinterpret_cast<const void*>(func), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 
 // Counters of kernel launches issued by this library (for the bench's gpu_launches claim).
 long long launch_count();

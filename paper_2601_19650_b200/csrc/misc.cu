@@ -5,6 +5,9 @@
 #include "kernels.h"
 #include "prof.h"
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -14,6 +17,19 @@ namespace tcbc {
 static std::atomic<long long> g_launches{0};
 long long launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
+
+void func_attr(const void* func, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int>, int> set;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(dev, func, (int)attr);
+  auto it = set.find(key);
+  if (it != set.end() && it->second >= value) return;
+  if (cudaFuncSetAttribute(func, attr, value) == cudaSuccess) set[key] = value;
+  else cudaGetLastError();
+}
 
 namespace {
 

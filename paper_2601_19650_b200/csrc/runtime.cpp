@@ -26,10 +26,14 @@ void* Arena::alloc(size_t bytes) {
   }
   size_t sz = std::max(bytes, chunk_);
   char* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, sz);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw Error(TTN_ERR_OOM, "device allocation of " + std::to_string(sz) + " bytes failed");
+  if (src_) {
+    p = static_cast<char*>(src_->get(sz));
+  } else {
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(TTN_ERR_OOM, "device allocation of " + std::to_string(sz) + " bytes failed");
+    }
   }
   chunks_.push_back(Chunk{p, sz, bytes});
   cur_ = chunks_.size() - 1;
@@ -45,7 +49,10 @@ void Arena::reset() {
 }
 
 void Arena::release() {
-  for (auto& c : chunks_) cudaFree(c.p);
+  for (auto& c : chunks_) {
+    if (src_) src_->put(c.p);
+    else cudaFree(c.p);
+  }
   chunks_.clear();
   cur_ = 0;
   live_ = 0;
@@ -157,19 +164,18 @@ ttn_s* new_ttn_like(ttn_ctx_s* ctx, const ttn_s* tmpl, int kind, const std::vect
   t->bond = bond;
   t->bond[t->root] = 1;
   finalize_shapes(t);
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&t->data), sizeof(cplx) * std::max<int64_t>(t->total, 1),
-                                  ctx->stream);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
+  try {
+    t->data = static_cast<cplx*>(ctx->get(sizeof(cplx) * std::max<int64_t>(t->total, 1)));
+  } catch (...) {
     delete t;
-    throw Error(TTN_ERR_OOM, "cudaMallocAsync of a TTN failed");
+    throw;
   }
   return t;
 }
 
 void free_ttn(ttn_s* t) {
   if (!t) return;
-  if (t->data) cudaFreeAsync(t->data, t->ctx ? t->ctx->stream : nullptr);
+  if (t->data && t->ctx) t->ctx->put(t->data);
   delete t;
 }
 
@@ -207,4 +213,52 @@ void ttn_ctx_s::ensure_small(size_t bytes) {
   size_t sz = std::max<size_t>(bytes, 1 << 20);
   TTN_CUDA(cudaMallocHost(&hbuf, sz));
   hbuf_size = sz;
+}
+
+void* ttn_ctx_s::get(size_t bytes) {
+  if (!pending_free.empty()) reap(false);
+  void* p = nullptr;
+  if (has_user_alloc) {
+    p = user_alloc.alloc(user_alloc.state, bytes, stream);
+    if (!p) throw tcbc::Error(TTN_ERR_OOM, "the caller's allocator returned NULL for " + std::to_string(bytes) + " bytes");
+    return p;
+  }
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw tcbc::Error(TTN_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  }
+  return p;
+}
+
+void ttn_ctx_s::put(void* p) {
+  if (!p) return;
+  if (!has_user_alloc) {
+    cudaFreeAsync(p, stream);
+    return;
+  }
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(ev, stream) != cudaSuccess) {
+    cudaGetLastError();
+    if (ev) cudaEventDestroy(ev);
+    cudaStreamSynchronize(stream);
+    user_alloc.free(user_alloc.state, p, stream);
+    return;
+  }
+  pending_free.emplace_back(ev, p);
+}
+
+void ttn_ctx_s::reap(bool all) {
+  size_t keep = 0;
+  for (size_t i = 0; i < pending_free.size(); ++i) {
+    auto& pf = pending_free[i];
+    const bool done = all ? (cudaEventSynchronize(pf.first), true) : cudaEventQuery(pf.first) == cudaSuccess;
+    if (done) {
+      user_alloc.free(user_alloc.state, pf.second, stream);
+      cudaEventDestroy(pf.first);
+    } else {
+      pending_free[keep++] = pf;
+    }
+  }
+  pending_free.resize(keep);
 }

@@ -27,12 +27,21 @@ struct Error : std::runtime_error {
                          std::string(#x) + ": " + cudaGetErrorString(e__));                  \
   } while (0)
 
+// Device memory source of a context: the caller's ttn_allocator, else a stream-ordered pool
+// owned by the context (cudaMallocFromPoolAsync on the ctx stream).
+struct MemSource {
+  virtual void* get(size_t bytes) = 0;
+  virtual void put(void* p) = 0;   // stream-ordered free (after the work enqueued so far)
+  virtual ~MemSource() {}
+};
+
 // Bump allocator over device chunks.  reset() recycles the memory for later work on the
 // SAME stream (stream order makes the reuse safe without a host sync).
 class Arena {
  public:
   explicit Arena(size_t chunk = 256ull << 20) : chunk_(chunk) {}
   ~Arena();
+  void set_source(MemSource* src) { src_ = src; }
   void* alloc(size_t bytes);
   void reset();
   void release();
@@ -42,6 +51,7 @@ class Arena {
   struct Chunk { char* p; size_t size; size_t used; };
   std::vector<Chunk> chunks_;
   size_t cur_ = 0, chunk_, high_ = 0, live_ = 0;
+  MemSource* src_ = nullptr;
 };
 
 // Pinned host ring mirrored in device memory; put() enqueues one H2D copy.
@@ -62,10 +72,22 @@ class RingStager : public Stager {
 
 }  // namespace tcbc
 
-struct ttn_ctx_s {
+struct ttn_ctx_s : tcbc::MemSource {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string last_error;
+  // device memory: the caller's allocator (ttn_ctx_create), else `pool` (owned by the root
+  // context; worker contexts share it).  Frees through a caller's allocator are deferred until
+  // the ctx stream has passed an event recorded at the free, so the allocator may hand the
+  // block to any stream at once.
+  ttn_allocator user_alloc{};
+  bool has_user_alloc = false;
+  cudaMemPool_t pool = nullptr;
+  bool owns_pool = false;
+  std::vector<std::pair<cudaEvent_t, void*>> pending_free;
+  void* get(size_t bytes) override;
+  void put(void* p) override;
+  void reap(bool all);   // hand completed deferred frees to the caller's allocator
   tcbc::RingStager* stager = nullptr;
   tcbc::Arena scratch;      // per-stage temporaries (reset between stages)
   tcbc::Arena env;          // per-apply environment factors (reset per apply)

@@ -45,3 +45,19 @@ def test_version_and_no_device_is_an_error(lib):
         pytest.skip("GPU present")
     with pytest.raises(P.TTNError):
         P.Context(0)
+
+
+def test_binding_checks_tensor_sizes_before_the_call():
+    """ttn_create refuses tensors whose size does not match the ABI shape from (parent, phys,
+    bond), before anything reaches the C side (no read past a short buffer)."""
+    import numpy as np
+    import paper_2601_19650_b200 as P
+    parent, phys, bond = [-1, 0, 0], [2, 2, 2], [1, 3, 4]
+    assert P.node_sizes(P.TTN_STATE, parent, phys, bond) == [2 * 1 * 3 * 4, 2 * 3, 2 * 4]
+    assert P.node_sizes(P.TTN_OPERATOR, parent, phys, bond) == [4 * 12, 4 * 3, 4 * 4]
+    good = [np.zeros((2, 1, 3, 4), complex), np.zeros((2, 3), complex), np.zeros((2, 4), complex)]
+    bad = good[:2] + [np.zeros((2, 3), complex)]
+    with pytest.raises(ValueError, match="node 2"):
+        P.ttn_create(None, P.TTN_STATE, parent, phys, bond, bad)
+    with pytest.raises(ValueError):
+        P.ttn_create(None, P.TTN_STATE, parent, phys, bond, good[:2])

@@ -151,3 +151,64 @@ def test_gram_orders_between_kernel_variants(P, ctx, chi, D, mb):
     parent = W.complete_binary(31)
     inst = W.configs.random_instance(parent, [2] * 31, chi, D, mb, seed=11)
     run_and_check(P, ctx, inst)
+
+
+def test_torch_caching_allocator_hook(P):
+    """ttn_allocator wired to PyTorch's caching allocator (SURVEY §8(b) PyTorch interop): the
+    library's workspaces and TTN handles come out of torch's pool (torch's allocated bytes grow
+    while handles live and return when they are destroyed), and the results are unchanged."""
+    import torch
+    base = torch.cuda.memory_allocated(0)
+    ctx = P.Context(0, allocator="torch")
+    try:
+        inst = W.make_config(3, seed=4)
+        op_g, st_g = gpu_pair(P, ctx, inst)
+        held = torch.cuda.memory_allocated(0) - base
+        n_in = sum(t.size for t in inst.state) + sum(t.size for t in inst.op)
+        assert held >= 16 * n_in
+        out, rep = P.cbc_apply(ctx, op_g, st_g, inst.max_bond)
+        phi_g = to_oracle(P, out, inst.parent)
+        op_o, psi_o = oracle_pair(inst)
+        phi_o = oracle_cbc(op_o, psi_o, inst.max_bond)
+        assert distances(phi_g, phi_o)[0] <= 1e-10
+        assert phi_g.bonds() == phi_o.bonds()
+        for h in (out, op_g, st_g):
+            h.destroy()
+    finally:
+        ctx.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated(0) == base
+
+
+def test_exact_factor_shortcut_and_its_fallback(P, ctx):
+    """untruncated compresses (tol = 0, max_bond >= min(m, n)) whose Gram is
+    certified full rank take the Cholesky factor instead of the eigensolver (report
+    exact_factors > 0), and the result is still exact (dense O psi).  A leaf with two equal
+    bond columns makes its up-Gram singular: the certificate fails, that compress goes
+    through the eigensolver and its bond drops to the numerical rank, like the oracle's."""
+    parent = [-1, 0, 0]
+    rng = np.random.default_rng(41)
+    st = [W.complex_gaussian(rng, (2, 1, 2, 3)), W.complex_gaussian(rng, (4, 2)), W.complex_gaussian(rng, (4, 3))]
+    st[1][:, 1] = st[1][:, 0]                         # rank-1 bond on edge (1, 0)
+    ops = [W.complex_gaussian(rng, (2, 2, 1, 1, 1)), W.complex_gaussian(rng, (4, 4, 1)), W.complex_gaussian(rng, (4, 4, 1))]
+    inst = Instance("rankdef", parent, [2, 4, 4], [1, 2, 3], [1, 1, 1], st, ops, 64)
+    phi_g, phi_o, rep, op_o, psi_o = _run_plain(P, ctx, inst)
+    assert phi_g.bonds() == phi_o.bonds()
+    assert phi_g.bonds()[1] == 1
+    ex = to_dense_operator(op_o) @ to_dense_state(psi_o)
+    assert np.linalg.norm(to_dense_state(phi_g) - ex) <= 1e-12 * np.linalg.norm(ex)
+    assert rep["exact_factors"] >= 1
+    # every compress of a generic untruncated binary tree is certified
+    inst = W.configs.random_instance(W.complete_binary(7), [2] * 7, 3, 2, 64, seed=8)
+    phi_g, phi_o, rep, op_o, psi_o = _run_plain(P, ctx, inst)
+    ex = to_dense_operator(op_o) @ to_dense_state(psi_o)
+    assert np.linalg.norm(to_dense_state(phi_g) - ex) <= 1e-12 * np.linalg.norm(ex)
+    assert phi_g.bonds() == phi_o.bonds()
+    assert rep["exact_factors"] >= 6, rep
+
+
+def _run_plain(P, ctx, inst):
+    op_g, st_g = gpu_pair(P, ctx, inst)
+    out, rep = P.cbc_apply(ctx, op_g, st_g, inst.max_bond)
+    op_o, psi_o = oracle_pair(inst)
+    return to_oracle(P, out, inst.parent), oracle_cbc(op_o, psi_o, inst.max_bond), rep, op_o, psi_o

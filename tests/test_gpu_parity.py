@@ -241,14 +241,24 @@ def test_large_gram_chebyshev_eigensolver(P, ctx, mb):
         assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
 
 
+def _isometries(phi):
+    for i, t in enumerate(phi.tensors):       # P3 on the GPU output
+        if i == phi.root:
+            continue
+        q = np.moveaxis(t, 1, -1).reshape(-1, t.shape[1])
+        assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
+
+
 def test_config4_t3ns_matches_oracle_golden(P, ctx):
-    """BASELINE config 4 (reading A12: 67-node T3NS, chi=128, D=16, max_bond=128) at full size.
-    The oracle needs ~6 min on 8 cores, so its results are stored by tests/golden/make_golden.py
-    (calls only oracle/): bonds, ||phi||^2 and every compress rank.  With the oracle's output
-    tensors present (tests/golden/cfg4_seed0_phi.npz, 88 MB, not in git) the gauge-invariant
-    distance is checked too."""
+    """BASELINE config 4 (reading A12: 67-node T3NS, chi=128, D=16, max_bond=128) at full size,
+    against the oracle run in this session (tests/bg_oracle.py, started when collection
+    finished so its ~5 CPU-minutes overlap the other GPU tests): gauge-invariant distance
+    1 - cos <= 1e-10 by the stable A18 form, identical bonds, ||phi||^2 within 1e-10 (A19's
+    sufficient condition for eps^2; ||O psi||^2 needs 2048-wide sweeps) and against the
+    committed golden (tests/golden/make_golden.py, oracle only), P3 on every output tensor."""
     import json
     import os
+    from .bg_oracle import bg_result
     gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg4_seed0.json")))
     inst = W.make_config(4, seed=0)
     op_g, st_g = gpu_pair(P, ctx, inst)
@@ -258,51 +268,51 @@ def test_config4_t3ns_matches_oracle_golden(P, ctx):
     n2 = norm(phi_g) ** 2
     assert abs(n2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"], (n2, gold["phi_norm2"])
     assert abs(rep["norm"] ** 2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"]
-    for i, t in enumerate(phi_g.tensors):       # P3
-        if i == phi_g.root:
-            continue
-        q = np.moveaxis(t, 1, -1).reshape(-1, t.shape[1])
-        assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
-    npz = os.path.join(os.path.dirname(__file__), "golden", "cfg4_seed0_phi.npz")
-    if os.path.exists(npz):
-        z = np.load(npz)
-        phi_o = TTN(inst.parent, [z[f"arr_{i}"] for i in range(len(inst.parent))], "state")
-        d_cos, d_rel = distances(phi_g, phi_o)
-        print(f"config 4 full parity: 1-cos={d_cos:.3e} rel={d_rel:.3e}")
-        assert d_cos <= 1e-10, (d_cos, d_rel)
+    _isometries(phi_g)
+    z = bg_result("cfg4")
+    phi_o = TTN(inst.parent, [z[f"n{i}"] for i in range(len(inst.parent))], "state")
+    assert phi_o.bonds() == gold["bonds"]
+    d_cos, d_rel = distances(phi_g, phi_o)
+    print(f"config 4 full parity: 1-cos={d_cos:.3e} rel={d_rel:.3e}")
+    assert d_cos <= 1e-10, (d_cos, d_rel)
+    assert abs(n2 - norm(phi_o) ** 2) <= 1e-10 * norm(phi_o) ** 2
 
 
 def test_config3_full_batch_as_benched(P, ctx):
     """Config 3 in bench.py's launch configuration (one cbc_apply_batch over seeds 0..63):
-    oracle parity on sampled instances, isometry (P3) and the report's norm on all 64."""
+    EVERY instance against the oracle (tests/bg_oracle.py, one process per instance):
+    1 - cos <= 1e-10 (A18), identical bonds, ||phi||^2 within 1e-10 relative (A19's sufficient
+    condition for |d eps^2| <= 1e-10, since ||phi|| <= ||O psi||; seeds 0..3 also check eps^2
+    against the exact ||O psi||^2 in test_config3_batch_matches_oracle), report norm, P3."""
+    from .bg_oracle import bg_result
     seeds = list(range(64))
     insts = [W.make_config(3, seed=s) for s in seeds]
     pairs = [gpu_pair(P, ctx, i) for i in insts]
     outs, reps = P.cbc_apply_batch(ctx, [p[0] for p in pairs], [p[1] for p in pairs], 32)
+    z = bg_result("cfg3")
+    worst = 0.0
     for s, (inst, out, rep) in enumerate(zip(insts, outs, reps)):
         phi_g = to_oracle(P, out, inst.parent)
-        if s in (0, 21, 42, 63):
-            op_o, psi_o = oracle_pair(inst)
-            _check(phi_g, oracle_cbc(op_o, psi_o, 32), op_o, psi_o, rep)
-            continue
-        for i, t in enumerate(phi_g.tensors):
-            if i == phi_g.root:
-                continue
-            q = np.moveaxis(t, 1, -1).reshape(-1, t.shape[1])
-            assert np.linalg.norm(q.conj().T @ q - np.eye(q.shape[1])) <= 1e-12
-        assert abs(rep["norm"] - np.linalg.norm(phi_g.tensors[phi_g.root])) <= 1e-12 * rep["norm"]
+        phi_o = TTN(inst.parent, [z[f"s{s}_n{i}"] for i in range(31)], "state")
+        d_cos, d_rel = distances(phi_g, phi_o)
+        worst = max(worst, d_cos)
+        assert d_cos <= 1e-10, (s, d_cos, d_rel)
+        assert phi_g.bonds() == phi_o.bonds(), s
+        assert abs(norm(phi_g) ** 2 - norm(phi_o) ** 2) <= 1e-10 * norm(phi_o) ** 2, s
+        assert abs(rep["norm"] - norm(phi_o)) <= 1e-10 * norm(phi_o), s
+        _isometries(phi_g)
+    print(f"config 3 batch of 64: worst 1-cos={worst:.3e}")
 
 
 def test_config5_full_batch_as_benched(P, ctx):
     """Config 5 in bench.py's launch configuration (64 seeds x 10 layers, 4 worker streams):
-    the untruncated layers keep ||phi|| = 1 for every seed (P13); sampled seeds vs oracle."""
+    the untruncated layers keep ||phi|| = 1 for every seed (P13); EVERY seed against the oracle
+    (tests/bg_oracle.py)."""
+    from .bg_oracle import bg_result
     seeds = list(range(64))
     parent = W.complete_binary(63)
     insts = [W.make_config(5, seed=s) for s in seeds]
     cur = [P.ttn_create(ctx, P.TTN_STATE, parent, i.phys, i.state_bond, i.state) for i in insts]
-    sample = {0: None, 63: None}
-    for s in sample:
-        sample[s] = TTN(parent, [t.copy() for t in insts[s].state])
     P.ttn_ctx_set_workers(ctx, 4)
     try:
         for layer in range(10):
@@ -310,17 +320,18 @@ def test_config5_full_batch_as_benched(P, ctx):
             for s in seeds:
                 o, ob, _ = W.circuit_layer_operator(parent, s, layer)
                 ops.append(P.ttn_create(ctx, P.TTN_OPERATOR, parent, [2] * 63, ob, o))
-                if s in sample:
-                    sample[s] = oracle_cbc(TTN(parent, o, "operator"), sample[s], 256)
             cur, reps = P.cbc_apply_batch(ctx, ops, cur, 256)
             for r in reps:
                 assert abs(r["norm"] - 1.0) <= 1e-12
     finally:
         P.ttn_ctx_set_workers(ctx, 1)
-    for s, po in sample.items():
+    z = bg_result("cfg5")
+    for s in seeds:
         g = to_oracle(P, cur[s], parent)
-        assert g.bonds() == po.bonds()
-        assert distances(g, po)[0] <= 1e-10
+        po = TTN(parent, [z[f"s{s}_n{i}"] for i in range(63)], "state")
+        assert g.bonds() == po.bonds(), s
+        d_cos, d_rel = distances(g, po)
+        assert d_cos <= 1e-10 and d_rel <= 1e-6, (s, d_cos, d_rel)
 
 
 def test_sandwich_and_op_norm2_match_oracle(P, ctx):

@@ -400,3 +400,70 @@ def test_A15_layer_operator_dense_matrix():
             ref[:, j] = _apply_gate_dense_all(ref[:, j].copy(), 7, gates)
         assert len(gates) >= 1
         assert np.linalg.norm(m - ref) < 1e-12 * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- A3 tol branch (reading A3)
+def _schmidt_pair(s, seed):
+    """Two-site chain (d = 4 each, root = site 0) whose only bond has Schmidt values s:
+    root T0[sigma, 1, a] = (U diag(s))[sigma, a], leaf T1[sigma, a] = V[sigma, a]^T with U, V
+    unitary, so the leaf is already an isometry toward the root (root-canonical form)."""
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(W.complex_gaussian(rng, (4, 4)))
+    v, _ = np.linalg.qr(W.complex_gaussian(rng, (4, 4)))
+    t0 = (u * np.asarray(s)[None, :])[:, None, :]
+    t1 = np.ascontiguousarray(v.T)
+    return TTN([-1, 0], [t0, t1])
+
+
+@pytest.mark.parametrize("tol,max_bond,k", [(0.45, 4, 2), (0.25, 4, 3), (0.05, 4, 4), (0.25, 2, 2),
+                                            (0.95, 4, 1), (0.0, 3, 3)])
+def test_A3_tol_keeps_sigma_above_tol_sigma1(tol, max_bond, k):
+    """Reading A3 ("setting a tolerance for the SVD"): keep min(max_bond, #{sigma_j >
+    tol sigma_1}).  The spectrum s = (1, .6, .3, .1) separates the readings: sigma > tol sigma_1
+    (A3), sigma^2 > tol sigma_1^2 and sigma > tol^2 sigma_1 give different bonds at tol = 0.45
+    (2, 1, 3) and 0.25 (3, 2, 3).  Identity TTNO on a root-canonical state: the result is the
+    dense truncated SVD, so the bond and eps^2 = dropped tail / total are fixed by the
+    spectrum alone (Eckart-Young, as in P6)."""
+    s = np.array([1.0, 0.6, 0.3, 0.1])
+    psi = _schmidt_pair(s, seed=17)
+    op = TTN([-1, 0], W.identity_operator([-1, 0], [4, 4]), "operator")
+    rec = {}
+    phi = cbc_apply(op, psi, max_bond, tol, record=rec)
+    assert phi.bonds() == [1, k]
+    v, w = to_dense_state(psi), to_dense_state(phi)
+    eps2 = np.linalg.norm(w - v) ** 2 / np.linalg.norm(v) ** 2
+    tail = np.sum(s[k:] ** 2) / np.sum(s ** 2)
+    assert abs(eps2 - tail) <= 1e-13
+    # the one compress (down factor of the leaf) reports the dropped weight sum_{j>k} s_j^2
+    assert len(rec["discarded"]) == 1
+    assert abs(rec["discarded"][0] - np.sum(s[k:] ** 2)) <= 1e-13
+    # the tensor-train oracle (Eqs. 5-9, written separately) takes the same decision
+    phi_tt = cbc_apply_tt(op, psi, max_bond, tol)
+    assert phi_tt.bonds() == [1, k]
+    assert np.linalg.norm(to_dense_state(phi_tt) - w) <= 1e-13
+
+
+def test_A3_tol_on_a_tree_matches_per_bond_dense_svd():
+    """tol on a 3-node star whose two bonds have prescribed spectra (root-canonical leaves):
+    each bond keeps #{sigma > tol sigma_1} of ITS spectrum, eps^2 is the dense projection error."""
+    rng = np.random.default_rng(23)
+    s1, s2 = np.array([1.0, 0.5, 0.2, 0.05]), np.array([1.0, 0.8, 0.08, 0.01])
+    # root core T0[s, 1, a, b] = u[s, (a, b)] s1[a] s2[b] with u unitary: the spectrum of
+    # bond a is s1 (times a constant), of bond b is s2
+    core = np.zeros((16, 4, 4), dtype=np.complex128)
+    u, _ = np.linalg.qr(W.complex_gaussian(rng, (16, 16)))
+    for a in range(4):
+        for b in range(4):
+            core[:, a, b] = u[:, 4 * a + b] * s1[a] * s2[b]
+    va, _ = np.linalg.qr(W.complex_gaussian(rng, (4, 4)))
+    vb, _ = np.linalg.qr(W.complex_gaussian(rng, (4, 4)))
+    psi = TTN([-1, 0, 0], [core[:, None], np.ascontiguousarray(va.T), np.ascontiguousarray(vb.T)])
+    op = TTN([-1, 0, 0], W.identity_operator([-1, 0, 0], [16, 4, 4]), "operator")
+    tol = 0.3
+    phi = cbc_apply(op, psi, 16, tol)
+    k1, k2 = int(np.sum(s1 > tol)), int(np.sum(s2 > tol))
+    assert phi.bonds() == [1, k1, k2] == [1, 2, 2]
+    v, w = to_dense_state(psi), to_dense_state(phi)
+    # product spectrum: the kept state is the (k1 x k2) block of s1 s2^T
+    kept = np.sum(np.outer(s1[:k1] ** 2, s2[:k2] ** 2))
+    assert abs(np.linalg.norm(w - v) ** 2 / np.linalg.norm(v) ** 2 - (1 - kept / np.sum(np.outer(s1 ** 2, s2 ** 2)))) <= 1e-13
