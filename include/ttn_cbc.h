@@ -67,6 +67,11 @@ typedef struct {
   int32_t exact_factors;       /* compresses taken by the exact-factor shortcut (untruncated,
                                   certified full rank: factor = Cholesky factor of the Gram, no
                                   eigensolver)                       */
+  double flops_gemm_exec;      /* flops issued to the complex GEMM kernel (all contraction,
+                                  Gram, factor, S, CholeskyQR and R products as executed)    */
+  double flops_gemm_min;       /* the same work at its algorithmic minimum: node contractions
+                                  at their cheapest pairwise order (the executed order may trade
+                                  flops for speed), Grams as Hermitian products (4 n^2 K)    */
 } ttn_cbc_report;
 
 /* ---------------------------------------------------------------- context             */
@@ -180,6 +185,22 @@ TTN_API ttn_status ttn_overlap_batch(ttn_ctx ctx, int32_t n, const ttn* a, const
  * Not combined with ttn_ctx_set_comm (a partitioned apply runs on ctx itself).  Errors: ARG. */
 TTN_API ttn_status ttn_ctx_set_workers(ttn_ctx ctx, int n);
 
+/* Schedule of cbc_apply / cbc_apply_batch on ctx (both on by default):
+ *  speculate = 1: with tol = 0 the host plans every compress with the generic rank
+ *    k = min(max_bond, m, n) and every QR of Eq. 13 as full rank, and the device checks
+ *    that the eigensolver / CholeskyQR agree; the apply then synchronises ONCE (for its
+ *    results) instead of once per tree level.  When a check fails (rank-deficient data, e.g.
+ *    circuit states) the result is discarded and the apply re-runs with the ranks read per
+ *    level; those shapes are not speculated again on this ctx.  tol > 0 and partitioned
+ *    (multi-GPU) applies always read ranks per level.
+ *  graphs = 1 (needs speculate): a successful speculative apply is captured as a CUDA graph
+ *    keyed by the shapes and the input handles' device addresses; a later apply with the same
+ *    key replays the graph (one launch, no host planning) and copies its outputs into fresh
+ *    handles.  Up to 8 graphs per ctx (least recently used evicted).  Applies that need the
+ *    Chebyshev solver (Grams of order > 512) synchronise inside and are not captured.
+ * Resets the graph cache.  Errors: ARG.                                                   */
+TTN_API ttn_status ttn_ctx_set_schedule(ttn_ctx ctx, int speculate, int graphs);
+
 /* ---------------------------------------------------------------- multi-GPU            */
 /* 128-byte NCCL unique id for a new communicator: create it on one rank and hand the same
  * bytes to every rank (e.g. by a torch.distributed broadcast).  NCCL is loaded at run time
@@ -204,6 +225,16 @@ TTN_API ttn_status ttn_comm_unique_id(void* out128);
  * 1-rank NCCL collectives): the single-GPU check of the schedule.  unique_id128 = NULL
  * detaches the communicator (plain applies).  Errors: ARG, NCCL.                          */
 TTN_API ttn_status ttn_ctx_set_comm(ttn_ctx ctx, const void* unique_id128, int rank, int world, int parts);
+/* In-process loopback group of `world` ranks for the same partitioned schedule on ONE device
+ * (tests, and machines with fewer GPUs than ranks): each rank is a ctx on its own stream,
+ * driven by its own host thread; collectives are host barriers between the rank threads plus
+ * stream-event dependencies and device copies / reductions (no kernel waits on another
+ * rank).  All ranks' contexts must be on the same device.  The group is reference counted:
+ * ttn_loopback_destroy drops the creator's reference.  Errors: ARG.                        */
+TTN_API ttn_status ttn_loopback_create(int world, void** group_out);
+TTN_API ttn_status ttn_loopback_destroy(void* group);
+/* ttn_ctx_set_comm with a loopback group instead of NCCL (same partition, same schedule). */
+TTN_API ttn_status ttn_ctx_set_comm_loopback(ttn_ctx ctx, void* group, int rank, int parts);
 /* The partition ttn_ctx_set_comm would use (host-only, no device needed): group_out[i] = -1
  * for nodes of the replicated top, else the subtree group of node i (rank = group % world).
  * Errors: ARG, TOPOLOGY.                                                                  */

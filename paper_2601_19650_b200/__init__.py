@@ -281,6 +281,11 @@ def ttn_norm(ctx: Context, a: TTN) -> float:
     return v.value
 
 
+def ttn_ctx_set_schedule(ctx: Context, speculate: bool = True, graphs: bool = True) -> None:
+    """Speculative ranks / CUDA-graph replay of cbc_apply on ctx (include/ttn_cbc.h)."""
+    L.check(ctx.h, L.load().ttn_ctx_set_schedule(ctx.h, int(bool(speculate)), int(bool(graphs))))
+
+
 def ttn_ctx_set_workers(ctx: Context, n: int) -> None:
     """Concurrent sub-batches for cbc_apply_batch (include/ttn_cbc.h); n = 1 turns it off."""
     L.check(ctx.h, L.load().ttn_ctx_set_workers(ctx.h, int(n)))
@@ -301,6 +306,31 @@ def ttn_ctx_set_comm(ctx: Context, unique_id: Optional[bytes], rank: int = 0, wo
         return
     buf = C.create_string_buffer(bytes(unique_id), 128)
     L.check(ctx.h, L.load().ttn_ctx_set_comm(ctx.h, buf, int(rank), int(world), int(parts)))
+
+
+class LoopbackGroup:
+    """In-process loopback communicator group (include/ttn_cbc.h ttn_loopback_create): the
+    partitioned multi-rank schedule with `world` contexts on one device, one host thread each."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        L.check(None, L.load().ttn_loopback_create(int(world), C.byref(h)))
+        self.h, self.world = h, world
+
+    def close(self):
+        if self.h:
+            L.load().ttn_loopback_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ttn_ctx_set_comm_loopback(ctx: Context, group: LoopbackGroup, rank: int, parts: int) -> None:
+    L.check(ctx.h, L.load().ttn_ctx_set_comm_loopback(ctx.h, group.h, int(rank), int(parts)))
 
 
 def ttn_partition_plan(parent: Sequence[int], parts: int) -> List[int]:

@@ -22,7 +22,8 @@ SYMBOLS = ["ttn_ctx_create", "ttn_ctx_destroy", "ttn_last_error", "ttn_version",
            "ttn_n_nodes", "ttn_node_shape", "ttn_get_tensor", "cbc_apply", "cbc_apply_batch", "ttn_overlap",
            "ttn_overlap_batch", "ttn_norm", "ttn_get_data", "ttn_get_data_batch", "ttn_profile_enable", "ttn_profile_read", "ttn_launch_count",
            "ttn_comm_unique_id", "ttn_ctx_set_comm", "ttn_partition_plan", "ttn_ctx_set_workers",
-           "ttn_sandwich", "ttn_op_norm2"]
+           "ttn_sandwich", "ttn_op_norm2", "ttn_ctx_set_schedule",
+           "ttn_loopback_create", "ttn_loopback_destroy", "ttn_ctx_set_comm_loopback"]
 
 
 class c128(C.Structure):
@@ -33,7 +34,7 @@ class Report(C.Structure):
     _fields_ = [("norm", C.c_double), ("discarded_weight_sum", C.c_double), ("max_bond", C.c_int64),
                 ("peak_entries", C.c_int64), ("seconds", C.c_double), ("flops_algorithmic", C.c_double),
                 ("rank_fallbacks", C.c_int32), ("host_syncs", C.c_int32), ("split_compresses", C.c_int32),
-                ("exact_factors", C.c_int32)]
+                ("exact_factors", C.c_int32), ("flops_gemm_exec", C.c_double), ("flops_gemm_min", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -89,6 +90,10 @@ def load():
         "ttn_launch_count": (C.c_int, [C.POINTER(I64)]),
         "ttn_comm_unique_id": (C.c_int, [P]),
         "ttn_ctx_set_workers": (C.c_int, [P, C.c_int]),
+        "ttn_ctx_set_schedule": (C.c_int, [P, C.c_int, C.c_int]),
+        "ttn_loopback_create": (C.c_int, [C.c_int, C.POINTER(P)]),
+        "ttn_loopback_destroy": (C.c_int, [P]),
+        "ttn_ctx_set_comm_loopback": (C.c_int, [P, P, C.c_int, C.c_int]),
         "ttn_sandwich": (C.c_int, [P, P, P, P, C.POINTER(c128)]),
         "ttn_op_norm2": (C.c_int, [P, P, P, C.POINTER(D)]),
         "ttn_ctx_set_comm": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int]),

@@ -69,6 +69,8 @@ ttn_status ctx_create_impl(int device, void* cuda_stream, const ttn_allocator* a
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     if (parent) {
+      c->speculate = parent->speculate;
+      c->graphs = parent->graphs;
       c->has_user_alloc = parent->has_user_alloc;
       c->user_alloc = parent->user_alloc;
       c->pool = parent->pool;
@@ -91,11 +93,12 @@ ttn_status ctx_create_impl(int device, void* cuda_stream, const ttn_allocator* a
     }
     c->scratch.set_source(c);
     c->env.set_source(c);
-    c->stager = new RingStager(c->stream);
+    c->ring = new RingStager(c->stream);
+    c->stager = c->ring;
     c->ensure_small(1 << 20);
   });
   if (s != TTN_OK) {
-    delete c->stager;
+    delete c->ring;
     if (c->owns_pool) cudaMemPoolDestroy(c->pool);
     delete c;
     return s;
@@ -115,13 +118,15 @@ ttn_status ttn_ctx_destroy(ttn_ctx ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto* w : ctx->workers) ttn_ctx_destroy(w);
   ctx->workers.clear();
+  graphs_release(ctx);
   ctx->scratch.release();
   ctx->env.release();
   cudaStreamSynchronize(ctx->stream);
   ctx->reap(true);
-  delete ctx->stager;
+  delete ctx->ring;
   delete ctx->comm;
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
+  if (ctx->spec_host) cudaFreeHost(ctx->spec_host);
   if (ctx->rank_ev) cudaEventDestroy(ctx->rank_ev);
   // outstanding TTN handles keep their blocks: the pool is released once they are freed
   if (ctx->owns_pool) cudaMemPoolDestroy(ctx->pool);
@@ -386,6 +391,22 @@ ttn_status ttn_ctx_set_workers(ttn_ctx ctx, int n) {
   });
 }
 
+ttn_status ttn_ctx_set_schedule(ttn_ctx ctx, int speculate, int graphs) {
+  if (!ctx) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    cudaStreamSynchronize(ctx->stream);
+    graphs_release(ctx);   // also forgets the shapes whose speculation failed
+    ctx->speculate = speculate != 0;
+    ctx->graphs = graphs != 0 && speculate != 0;
+    for (auto* w : ctx->workers) {
+      graphs_release(w);
+      w->speculate = ctx->speculate;
+      w->graphs = ctx->graphs;
+    }
+  });
+}
+
 ttn_status ttn_comm_unique_id(void* out128) {
   if (!out128) return TTN_ERR_ARG;
   return guard(nullptr, [&] { comm_unique_id(out128); });
@@ -402,6 +423,37 @@ ttn_status ttn_ctx_set_comm(ttn_ctx ctx, const void* unique_id128, int rank, int
     if (!unique_id128) return;
     if (world < 1 || rank < 0 || rank >= world || parts < world) throw Error(TTN_ERR_ARG, "need 0 <= rank < world <= parts");
     ctx->comm = comm_create(unique_id128, rank, world, ctx->device);
+    ctx->parts = parts;
+  });
+}
+
+ttn_status ttn_loopback_create(int world, void** group_out) {
+  if (!group_out || world < 1) return TTN_ERR_ARG;
+  *group_out = nullptr;
+  return guard(nullptr, [&] { *group_out = loop_group_create(world); });
+}
+
+ttn_status ttn_loopback_destroy(void* group) {
+  if (!group) return TTN_ERR_ARG;
+  loop_group_release(static_cast<LoopGroup*>(group));
+  return TTN_OK;
+}
+
+ttn_status ttn_ctx_set_comm_loopback(ttn_ctx ctx, void* group, int rank, int parts) {
+  if (!ctx || !group) return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    LoopGroup* lg = static_cast<LoopGroup*>(group);
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx->comm;
+    ctx->comm = nullptr;
+    ctx->parts = 1;
+    Comm* c = loop_comm_create(lg, rank, ctx->device);
+    if (parts < c->world) {
+      delete c;
+      throw Error(TTN_ERR_ARG, "need parts >= world");
+    }
+    ctx->comm = c;
     ctx->parts = parts;
   });
 }

@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <memory>
+#include <set>
 
 namespace tcbc {
 
@@ -57,6 +59,40 @@ struct QRJob {
   cplx* Q;           // m x r output, r = min(m, kd)
   int inst;
   int* exp = nullptr;   // max binary exponent of S, written by the producing GEMM
+};
+
+// Per-instance flop counts (8 per complex MAC).  `all` is the report's flops_algorithmic;
+// `nongemm` the eigensolver / Cholesky proxies inside it; cx_exec / cx_min the node
+// contractions as executed / at the cheapest pairwise order (the roofline's algorithmic work).
+struct FlopAcc {
+  double all = 0.0, nongemm = 0.0, cx_exec = 0.0, cx_min = 0.0;
+  FlopAcc& operator+=(double v) {   // a GEMM issued as is (Gram, factor, S, QR, R)
+    all += v;
+    return *this;
+  }
+  void add_nongemm(double v) {
+    all += v;
+    nongemm += v;
+  }
+  void add_contract(double exec, double mn) {
+    all += exec;
+    cx_exec += exec;
+    cx_min += mn;
+  }
+  double gemm_exec() const { return all - nongemm; }
+  double gemm_min() const { return all - nongemm - (cx_exec - cx_min); }
+};
+
+// Device side of a speculative apply (no host synchronisation inside the sweeps): the host
+// plans every compress with k = kmax and every QR as full rank; the device accumulates the
+// discarded weights / exact-factor counts per instance and raises `flag` when a rank differs
+// (1), a weight is not finite (2) or a CholeskyQR pivot fails (4) -- the caller then discards
+// the result and re-runs the apply with synchronised ranks.
+struct SpecDev {
+  double* wacc;   // [nb]
+  int* xacc;      // [nb]
+  int* flag;
+  bool* host_synced;   // set when a stage had to synchronise anyway (Chebyshev solver)
 };
 
 Task node_task(const ttn_s* st, const ttn_s* op, int i, const std::map<int, const Fac*>& facs, int open_leg,
@@ -98,8 +134,8 @@ void check_heev_size(int64_t nn) {
 
 // Gram -> eigenpairs -> factor, for every job; synchronises once to read the ranks.
 void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_bond, double tol,
-                    ExecStats& st, std::vector<double>& w_inst, std::vector<double>& flops_inst,
-                    std::vector<int>& exact_inst) {
+                    ExecStats& st, std::vector<double>& w_inst, std::vector<FlopAcc>& flops_inst,
+                    std::vector<int>& exact_inst, const SpecDev* spec) {
   if (jobs.empty()) return;
   HostScope hs_("compress_batch");
   const int nj = (int)jobs.size();
@@ -155,7 +191,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     h.exp2 = ej;
     p2[j] = Pow2Problem{const_cast<cplx*>(J.X), m * n, ej};
     h.max_bond = (int)std::min<int64_t>(max_bond, INT32_MAX);
-    flops_inst[J.inst] += 8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * kmax);
+    flops_inst[J.inst].add_nongemm(8.0 * ((4.0 / 3.0) * nn * nn * nn + 2.0 * nn * nn * kmax));
     // factor storage (kmax rows; the first k are the factor)
     J.dst->p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * kmax * n));
     J.dst->a = J.a;
@@ -207,6 +243,31 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     launch_potrf(cpot.data(), (int)cpot.size(), *ctx->stager, ctx->stream);
     launch_trtri(ctri.data(), (int)ctri.size(), *ctx->stager, ctx->stream);
     launch_chol_certify(ccert.data(), (int)ccert.size(), *ctx->stager, ctx->stream);
+  }
+  if (spec) {   // speculative: k = kmax, checked on the device (no host read, no sync)
+    {
+      std::vector<HeevProblem> small;
+      std::vector<HeevProblem*> large;
+      for (auto& h : hp) {
+        if (chfsi_applicable(h.n, h.kmax)) large.push_back(&h);
+        else small.push_back(h);
+      }
+      if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream);
+      if (!large.empty()) {
+        *spec->host_synced = true;
+        chfsi_heev(ctx, large, st);
+      }
+    }
+    if (!sr.empty()) launch_scale_rows(sr.data(), (int)sr.size(), *ctx->stager, ctx->stream);
+    gemm_batch(ctx, fgemm, st);
+    launch_exact_factor(cfac.data(), (int)cfac.size(), *ctx->stager, ctx->stream);
+    std::vector<SpecCheck> sc(nj);
+    for (int j = 0; j < nj; ++j) {
+      sc[j] = SpecCheck{d_k + j, d_w + j, d_skip + j, (int)kmaxs[j], jobs[j].inst};
+      jobs[j].dst->k = kmaxs[j];
+    }
+    launch_spec_check(sc.data(), nj, spec->wacc, spec->xacc, spec->flag, *ctx->stager, ctx->stream);
+    return;
   }
   // ranks and discarded weights go to the host as soon as the eigenvalue stages have fixed them:
   // the host waits on that point only, and builds the next level while the eigenvector stages
@@ -264,8 +325,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
 }
 
 // CholeskyQR2 of every S (m > kd); Q = I for m <= kd.  Synchronises once for pivot flags.
-int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vector<double>& flops_inst,
-             std::vector<int>& fb_inst) {
+int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vector<FlopAcc>& flops_inst,
+             std::vector<int>& fb_inst, const SpecDev* spec) {
   if (jobs.empty()) return 0;
   HostScope hs_("qr_batch");
   std::vector<EyeProblem> eyes;
@@ -274,6 +335,7 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
   std::vector<TrtriProblem> t1, t2;
   std::vector<int> tall;
   int* d_info = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * 2 * jobs.size()));
+  TTN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int) * 2 * jobs.size(), ctx->stream));   // Q = I jobs stay 0
   for (size_t j = 0; j < jobs.size(); ++j) {
     QRJob& J = jobs[j];
     if (J.m <= J.kd) {
@@ -303,7 +365,7 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
     p2.push_back(PotrfProblem{W2, k, (int)k, 0, d_info + 2 * j + 1, kCholTol * 1e-2});
     t2.push_back(TrtriProblem{W2, Li2, k, (int)k, 0});
     g4.push_back(gp(Q1, OP_N, k, Li2, OP_C, k, J.Q, m, k, k));       // Q = Q1 L2^{-H}
-    flops_inst[J.inst] += 8.0 * 2.0 * (k * k * k / 3.0);
+    flops_inst[J.inst].add_nongemm(8.0 * 2.0 * (k * k * k / 3.0));
   }
   if (!eyes.empty()) launch_eye(eyes.data(), (int)eyes.size(), *ctx->stager, ctx->stream);
   if (tall.empty()) return 0;
@@ -326,6 +388,10 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
   launch_potrf(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
   launch_trtri(t2.data(), (int)t2.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, g4, st);
+  if (spec) {   // speculative: a pivot failure (rank-deficient S) invalidates the apply
+    launch_flag_nonzero(d_info, 2 * (int)jobs.size(), spec->flag, 4, ctx->stream);
+    return 0;
+  }
   ctx->ensure_small(sizeof(int) * 2 * jobs.size());
   int* hi = reinterpret_cast<int*>(ctx->hbuf);
   TTN_CUDA(cudaMemcpyAsync(hi, d_info, sizeof(int) * 2 * jobs.size(), cudaMemcpyDeviceToHost, ctx->stream));
@@ -337,7 +403,7 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
       QRJob& J = jobs[j];
       cplx* tau = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * J.kd));
       fb.push_back(GeqrProblem{const_cast<cplx*>(J.S), J.Q, tau, (int)J.m, (int)J.kd});
-      flops_inst[J.inst] += 8.0 * 2.0 * (double)J.m * J.kd * J.kd;
+      flops_inst[J.inst].add_nongemm(8.0 * 2.0 * (double)J.m * J.kd * J.kd);
       fb_inst[J.inst] += 1;
     }
   if (!fb.empty()) launch_geqr_q(fb.data(), (int)fb.size(), *ctx->stager, ctx->stream);
@@ -413,9 +479,39 @@ Partition make_partition(const ttn_s* ref, const ttn_ctx_s* ctx) {
   return P;
 }
 
-void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts, int64_t max_bond,
-                    double tol, ttn_s** outs, ttn_cbc_report* reps) {
+namespace {
+
+enum class Mode { Sync, Spec, Capture };
+
+// Control block of one pass of the schedule.  Sync: ranks read by the host per level (the
+// general path).  Spec / Capture: speculative ranks, no host synchronisation; the per-instance
+// results (norms, discarded weights, exact-factor counts, the flag) are copied into
+// `host_res` at the end (layout of SpecRes) and the caller synchronises and checks them.
+struct CoreCtl {
+  Mode mode = Mode::Sync;
+  char* host_res = nullptr;                     // pinned, SpecRes::bytes(nb)
+  std::function<cplx*(int64_t)> out_alloc;      // Capture: outputs in the graph's buffer
+  bool host_synced = false;                     // a stage synchronised anyway (no capture)
+  int64_t out_elems = 0;                        // entries of all outputs
+  // host-side per-instance results (known from shapes alone in the speculative modes)
+  std::vector<FlopAcc> flops;
+  std::vector<int64_t> maxb;
+  int64_t peak = 0;
+};
+
+// layout of the speculative result block (device: env arena; host: pinned)
+struct SpecRes {
+  static size_t bytes(int nb) { return sizeof(double) * 2 * nb + sizeof(int) * (nb + 1); }
+  static double* sq(char* p, int nb) { (void)nb; return reinterpret_cast<double*>(p); }
+  static double* w(char* p, int nb) { return reinterpret_cast<double*>(p) + nb; }
+  static int* x(char* p, int nb) { return reinterpret_cast<int*>(reinterpret_cast<double*>(p) + 2 * nb); }
+  static int* flag(char* p, int nb) { return x(p, nb) + nb; }
+};
+
+void apply_core(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts, int64_t max_bond,
+                double tol, ttn_s** outs, ttn_cbc_report* reps, CoreCtl& cc) {
   auto t0 = std::chrono::steady_clock::now();
+  const bool specm = cc.mode != Mode::Sync;
   if (nb <= 0) throw Error(TTN_ERR_ARG, "batch size must be >= 1");
   if (max_bond < 1) throw Error(TTN_ERR_ARG, "max_bond must be >= 1");
   if (!(tol >= 0.0 && tol < 1.0)) throw Error(TTN_ERR_ARG, "tol must be in [0, 1)");
@@ -453,9 +549,19 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   ctx->host_syncs = 0;
   ctx->sync_wait_s = 0.0;
   ExecStats st;
+  // speculative modes: device accumulators and the result block (zeroed in stream order)
+  char* d_res = nullptr;
+  SpecDev sdev{};
+  if (specm) {
+    d_res = static_cast<char*>(ctx->env.alloc(SpecRes::bytes(nb)));
+    TTN_CUDA(cudaMemsetAsync(d_res, 0, SpecRes::bytes(nb), ctx->stream));
+    sdev = SpecDev{SpecRes::w(d_res, nb), SpecRes::x(d_res, nb), SpecRes::flag(d_res, nb), &cc.host_synced};
+  }
+  const SpecDev* spec = specm ? &sdev : nullptr;
   // per-instance accumulators: replicated top work counted on every rank, subtree work only
   // on its owner (summed over ranks at the end)
-  std::vector<double> w_inst(nb, 0.0), flops_inst(nb, 0.0), w_sub(nb, 0.0), flops_sub(nb, 0.0);
+  std::vector<double> w_inst(nb, 0.0), w_sub(nb, 0.0);
+  std::vector<FlopAcc> flops_inst(nb), flops_sub(nb);
   std::vector<int> fb_inst(nb, 0), fb_sub(nb, 0), split_inst(nb, 0), exact_inst(nb, 0), exact_sub(nb, 0);
   std::vector<Fac> up((size_t)nb * n), down((size_t)nb * n), R((size_t)nb * n);
   // trivial factor L^{[(-,r)]} = 1 (extent-1 legs)
@@ -464,7 +570,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   for (int b = 0; b < nb; ++b) down[(size_t)b * n + root] = Fac{one, 1, 1, 1};
 
   auto acc_w = [&](bool sub) -> std::vector<double>& { return sub ? w_sub : w_inst; };
-  auto acc_f = [&](bool sub) -> std::vector<double>& { return sub ? flops_sub : flops_inst; };
+  auto acc_f = [&](bool sub) -> std::vector<FlopAcc>& { return sub ? flops_sub : flops_inst; };
   auto acc_x = [&](bool sub) -> std::vector<int>& { return sub ? exact_sub : exact_inst; };
 
   // ---------------- row split of the replicated top's heavy compresses (partitioned apply):
@@ -524,7 +630,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
     for (size_t q = 0; q < sl_t.size(); ++q) sl_t[q].out_exp = d_e + sl_job[q];
     ExecStats cs;
     if (!sl_t.empty()) contract_batch(ctx, sl_t, cs);
-    for (size_t q = 0; q < sl_t.size(); ++q) flops_sub[sp_j[sl_job[q]].inst] += sl_t[q].flops;
+    for (size_t q = 0; q < sl_t.size(); ++q) flops_sub[sp_j[sl_job[q]].inst].add_contract(sl_t[q].flops, sl_t[q].flops_min);
     st.flops += cs.flops;
     st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
     comm->allreduce_max(d_e, ns, ctx->stream);
@@ -565,7 +671,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       sp_j[q].exp = d_e + q;
       sp_j[q].X = nullptr;
     }
-    compress_batch(ctx, sp_j, max_bond, tol, st, w_inst, flops_inst, exact_inst);
+    compress_batch(ctx, sp_j, max_bond, tol, st, w_inst, flops_inst, exact_inst, spec);
   };
 
   // ---------------- 1. up-sweep (Eq. 10) over the nodes selected by `sel`, deepest level first
@@ -602,9 +708,9 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
         jobs[j].m = tot / jobs[j].n;
       }
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-      for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst] += tasks[j].flops;
+      for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst].add_contract(tasks[j].flops, tasks[j].flops_min);
       st.flops += cs.flops;
-      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub));
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub), spec);
       ctx->scratch.reset();
     }
   };
@@ -646,9 +752,9 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
         jobs[j].m = tot / jobs[j].n;
       }
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-      for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst] += tasks[j].flops;
+      for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst].add_contract(tasks[j].flops, tasks[j].flops_min);
       st.flops += cs.flops;
-      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub));
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub), spec);
       ctx->scratch.reset();
     }
   };
@@ -727,7 +833,10 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
         rb[b][i] = std::min<int64_t>(ms, down[(size_t)b * n + i].k);
       }
   }
-  for (int b = 0; b < nb; ++b) outs[b] = new_ttn_like(ctx, ref, TTN_STATE, rb[b]);
+  for (int b = 0; b < nb; ++b) {
+    outs[b] = new_ttn_like(ctx, ref, TTN_STATE, rb[b], cc.out_alloc);
+    cc.out_elems += outs[b]->total;
+  }
 
   // ---------------- 3. final sweep (Eqs. 12-14) and 4. assembly, over the nodes selected
   auto final_sweep = [&](auto sel, bool sub) {
@@ -748,7 +857,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       ExecStats cs;
       contract_batch(ctx, tasks, cs);
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
-      for (size_t j = 0; j < who.size(); ++j) acc_f(sub)[who[j].first] += tasks[j].flops;
+      for (size_t j = 0; j < who.size(); ++j) acc_f(sub)[who[j].first].add_contract(tasks[j].flops, tasks[j].flops_min);
       st.flops += cs.flops;
       std::vector<GemmProblem> sg, rg;
       std::vector<QRJob> qj;
@@ -786,7 +895,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
         acc_f(sub)[b] += 8.0 * (double)r * nz * ms;
       }
       gemm_batch(ctx, sg, st);
-      qr_batch(ctx, qj, st, acc_f(sub), sub ? fb_sub : fb_inst);
+      qr_batch(ctx, qj, st, acc_f(sub), sub ? fb_sub : fb_inst, spec);
       if (!pq.empty()) launch_permute(pq.data(), (int)pq.size(), *ctx->stager, ctx->stream);
       gemm_batch(ctx, rg, st);
       ctx->scratch.reset();
@@ -809,7 +918,7 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
 
   // ---------------- report: ||phi|| = ||T'_root||_F; subtree totals summed over ranks
   std::vector<SumsqProblem> sq(nb);
-  double* d_sq = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nb * 5));
+  double* d_sq = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nb * 8));
   for (int b = 0; b < nb; ++b) {
     sq[b].x = outs[b]->node(root);
     sq[b].len = 1;
@@ -817,23 +926,40 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
     sq[b].out = d_sq + b;
   }
   launch_sumsq(sq.data(), nb, *ctx->stager, ctx->stream);
+  if (specm) {   // results to the caller's pinned block; the caller synchronises and checks
+    TTN_CUDA(cudaMemcpyAsync(d_res, d_sq, sizeof(double) * nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(cc.host_res, d_res, SpecRes::bytes(nb), cudaMemcpyDeviceToHost, ctx->stream));
+    cc.flops = flops_inst;
+    cc.maxb.assign(nb, 1);
+    for (int b = 0; b < nb; ++b)
+      for (int i = 0; i < n; ++i) cc.maxb[b] = std::max<int64_t>(cc.maxb[b], rb[b][i]);
+    cc.peak = st.peak_entries;
+    return;
+  }
   if (part.on) {
-    std::vector<double> h(4 * (size_t)nb);
+    constexpr int NF = 7;
+    std::vector<double> h(NF * (size_t)nb);
     for (int b = 0; b < nb; ++b) {
       h[b] = w_sub[b];
-      h[nb + b] = flops_sub[b];
+      h[nb + b] = flops_sub[b].all;
       h[2 * nb + b] = fb_sub[b];
       h[3 * nb + b] = exact_sub[b];
+      h[4 * nb + b] = flops_sub[b].nongemm;
+      h[5 * nb + b] = flops_sub[b].cx_exec;
+      h[6 * nb + b] = flops_sub[b].cx_min;
     }
-    TTN_CUDA(cudaMemcpyAsync(d_sq + nb, h.data(), sizeof(double) * 4 * nb, cudaMemcpyHostToDevice, ctx->stream));
-    comm->allreduce_sum(d_sq + nb, 4 * (size_t)nb, ctx->stream);
-    TTN_CUDA(cudaMemcpyAsync(h.data(), d_sq + nb, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(d_sq + nb, h.data(), sizeof(double) * NF * nb, cudaMemcpyHostToDevice, ctx->stream));
+    comm->allreduce_sum(d_sq + nb, NF * (size_t)nb, ctx->stream);
+    TTN_CUDA(cudaMemcpyAsync(h.data(), d_sq + nb, sizeof(double) * NF * nb, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
     for (int b = 0; b < nb; ++b) {
       w_inst[b] += h[b];
-      flops_inst[b] += h[nb + b];
+      flops_inst[b].all += h[nb + b];
       fb_inst[b] += (int)std::lround(h[2 * nb + b]);
       exact_inst[b] += (int)std::lround(h[3 * nb + b]);
+      flops_inst[b].nongemm += h[4 * nb + b];
+      flops_inst[b].cx_exec += h[5 * nb + b];
+      flops_inst[b].cx_min += h[6 * nb + b];
     }
   }
   ctx->ensure_small(sizeof(double) * nb);
@@ -862,12 +988,313 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
       for (int i = 0; i < n; ++i) r.max_bond = std::max<int64_t>(r.max_bond, rb[b][i]);
       r.peak_entries = st.peak_entries;
       r.seconds = secs;
-      r.flops_algorithmic = flops_inst[b];
+      r.flops_algorithmic = flops_inst[b].all;
+      r.flops_gemm_exec = flops_inst[b].gemm_exec();
+      r.flops_gemm_min = flops_inst[b].gemm_min();
       r.rank_fallbacks = fb_inst[b];
       r.host_syncs = ctx->host_syncs;
       r.split_compresses = split_inst[b];
       r.exact_factors = exact_inst[b];
     }
+  }
+}
+
+// ---------------------------------------------------------------- speculative schedule + graphs
+// "captures CUDA graphs when ranks are static".  With tol = 0 the ranks of a
+// generic apply are min(max_bond, m, n), known from the shapes alone; the schedule is planned
+// with those ranks and checked on the device (SpecDev), so an apply needs ONE host
+// synchronisation (its results) instead of one per level.  A speculative apply that succeeded
+// is captured as a CUDA graph (keyed by shapes and input addresses) and later applies on the
+// same inputs replay it: no host planning, one graph launch.  A failed check (rank-deficient
+// or tolerance-truncated data) discards the result and re-runs the synchronised schedule;
+// those shapes are then never speculated again on this ctx.
+struct GraphEntry {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  char* desc = nullptr;           // device descriptors of every launch (uploaded once)
+  cplx* outbuf = nullptr;         // the outputs, copied to fresh handles after each replay
+  char* host = nullptr;           // pinned result block (SpecRes)
+  std::vector<ttn_s*> tmpl;       // output shapes; data points into outbuf (not owned)
+  std::vector<FlopAcc> flops;
+  std::vector<int64_t> maxb;
+  int64_t peak = 0;
+  long long launches = 0;         // kernels per replay
+  ProfSink sink;
+  uint64_t last_use = 0;
+};
+
+}  // namespace
+
+struct GraphCache {
+  std::map<std::vector<int64_t>, std::unique_ptr<GraphEntry>> map;
+  std::set<std::vector<int64_t>> failed;    // trees whose speculation failed: always synchronised
+  std::set<std::vector<int64_t>> nograph;   // keys whose capture failed
+  std::set<std::vector<int64_t>> seen;      // keys with one successful speculative apply
+  uint64_t tick = 0;
+};
+
+namespace {
+
+void destroy_entry(ttn_ctx_s* ctx, GraphEntry* e) {
+  if (e->ex) cudaGraphExecDestroy(e->ex);
+  if (e->g) cudaGraphDestroy(e->g);
+  if (e->desc) cudaFree(e->desc);
+  if (e->outbuf) ctx->put(e->outbuf);
+  if (e->host) cudaFreeHost(e->host);
+  for (auto* t : e->tmpl) delete t;   // data belongs to outbuf
+  e->tmpl.clear();
+}
+
+GraphCache& graphs_of(ttn_ctx_s* ctx) {
+  if (!ctx->gr) ctx->gr = new GraphCache();
+  return *ctx->gr;
+}
+
+std::vector<int64_t> shape_key(int nb, const ttn_s* const* ops, const ttn_s* const* sts, int64_t max_bond) {
+  const ttn_s* ref = sts[0];
+  std::vector<int64_t> k{nb, max_bond, ref->n};
+  for (int i = 0; i < ref->n; ++i) {
+    k.push_back(ref->parent[i]);
+    k.push_back(ref->phys[i]);
+  }
+  for (int b = 0; b < nb; ++b)
+    for (int i = 0; i < ref->n; ++i) {
+      k.push_back(sts[b]->bond[i]);
+      k.push_back(ops[b]->bond[i]);
+    }
+  return k;
+}
+
+void fill_reports(ttn_cbc_report* reps, int nb, char* host, const std::vector<FlopAcc>& flops,
+                  const std::vector<int64_t>& maxb, int64_t peak, double secs, int syncs) {
+  if (!reps) return;
+  for (int b = 0; b < nb; ++b) {
+    ttn_cbc_report& r = reps[b];
+    r.norm = std::sqrt(SpecRes::sq(host, nb)[b]);
+    r.discarded_weight_sum = SpecRes::w(host, nb)[b];
+    r.max_bond = maxb[b];
+    r.peak_entries = peak;
+    r.seconds = secs;
+    r.flops_algorithmic = flops[b].all;
+    r.flops_gemm_exec = flops[b].gemm_exec();
+    r.flops_gemm_min = flops[b].gemm_min();
+    r.rank_fallbacks = 0;
+    r.host_syncs = syncs;
+    r.split_compresses = 0;
+    r.exact_factors = SpecRes::x(host, nb)[b];
+  }
+}
+
+bool spec_ok(char* host, int nb) {
+  if (*SpecRes::flag(host, nb) != 0) return false;
+  for (int b = 0; b < nb; ++b)
+    if (!std::isfinite(SpecRes::sq(host, nb)[b])) return false;
+  return true;
+}
+
+// Capture the speculative schedule as a graph (after a successful uncaptured run that sized
+// the descriptor and output buffers).  Returns null if the capture is not possible.
+std::unique_ptr<GraphEntry> capture(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts,
+                                    int64_t max_bond, size_t desc_bytes, int64_t out_elems) {
+  std::unique_ptr<GraphEntry> e(new GraphEntry());
+  const size_t cap = desc_bytes + (1u << 16);
+  if (cudaMalloc(&e->desc, cap) != cudaSuccess) {
+    cudaGetLastError();
+    e->desc = nullptr;
+    return nullptr;
+  }
+  if (cudaMallocHost(&e->host, SpecRes::bytes(nb)) != cudaSuccess) {
+    cudaGetLastError();
+    e->host = nullptr;
+    destroy_entry(ctx, e.get());
+    return nullptr;
+  }
+  try {
+    e->outbuf = static_cast<cplx*>(ctx->get(sizeof(cplx) * std::max<int64_t>(out_elems, 1)));
+  } catch (...) {
+    destroy_entry(ctx, e.get());
+    return nullptr;
+  }
+  TTN_CUDA(cudaStreamSynchronize(ctx->stream));   // outbuf allocation complete before capture
+  CaptureStager cs(e->desc, cap);
+  int64_t used = 0;
+  CoreCtl cc;
+  cc.mode = Mode::Capture;
+  cc.host_res = e->host;
+  cc.out_alloc = [&](int64_t elems) -> cplx* {
+    if (used + elems > out_elems) throw Error(TTN_ERR_UNSUPPORTED, "graph output buffer too small");
+    cplx* p = e->outbuf + used;
+    used += elems;
+    return p;
+  };
+  std::vector<ttn_s*> outs(nb, nullptr);
+  const long long lc0 = launch_count();
+  ctx->stager = &cs;
+  ctx->scratch.frozen = ctx->env.frozen = true;
+  ctx->capturing = true;
+  const bool prof = prof_on();
+  if (prof) prof_set_sink(&e->sink);
+  bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    try {
+      apply_core(ctx, nb, ops, sts, max_bond, 0.0, outs.data(), nullptr, cc);
+    } catch (...) {
+      ok = false;
+    }
+    cudaGraph_t g = nullptr;
+    const bool ended = cudaStreamEndCapture(ctx->stream, &g) == cudaSuccess;
+    ok = ok && ended && g && !cc.host_synced;
+    if (g && !ok) cudaGraphDestroy(g);
+    if (ok) e->g = g;
+  }
+  cudaGetLastError();
+  if (prof) prof_set_sink(nullptr);
+  ctx->capturing = false;
+  ctx->scratch.frozen = ctx->env.frozen = false;
+  ctx->stager = ctx->ring;
+  e->launches = launch_count() - lc0;
+  add_launches(-e->launches);   // captured, not launched
+  e->tmpl = outs;
+  if (!ok) {
+    destroy_entry(ctx, e.get());
+    return nullptr;
+  }
+  TTN_CUDA(cudaMemcpy(e->desc, cs.shadow.data(), cs.shadow.size(), cudaMemcpyHostToDevice));
+  if (cudaGraphInstantiate(&e->ex, e->g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    e->ex = nullptr;
+    destroy_entry(ctx, e.get());
+    return nullptr;
+  }
+  e->flops = cc.flops;
+  e->maxb = cc.maxb;
+  e->peak = cc.peak;
+  return e;
+}
+
+// one replay; false when the device check failed (outputs discarded)
+bool replay(ttn_ctx_s* ctx, GraphEntry* e, int nb, const ttn_s* ref, ttn_s** outs, ttn_cbc_report* reps) {
+  auto t0 = std::chrono::steady_clock::now();
+  ctx->host_syncs = 0;
+  TTN_CUDA(cudaGraphLaunch(e->ex, ctx->stream));
+  add_launches(e->launches);
+  for (int b = 0; b < nb; ++b) {
+    outs[b] = new_ttn_like(ctx, ref, TTN_STATE, e->tmpl[b]->bond);
+    TTN_CUDA(cudaMemcpyAsync(outs[b]->data, e->tmpl[b]->data, sizeof(cplx) * e->tmpl[b]->total,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ctx->sync();
+  prof_replay(e->sink);
+  if (!spec_ok(e->host, nb)) {
+    for (int b = 0; b < nb; ++b) {
+      free_ttn(outs[b]);
+      outs[b] = nullptr;
+    }
+    return false;
+  }
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  fill_reports(reps, nb, e->host, e->flops, e->maxb, e->peak, secs, ctx->host_syncs);
+  return true;
+}
+
+}  // namespace
+
+void graphs_release(ttn_ctx_s* ctx) {
+  if (!ctx->gr) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->gr->map) destroy_entry(ctx, kv.second.get());
+  delete ctx->gr;
+  ctx->gr = nullptr;
+}
+
+void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts, int64_t max_bond,
+                    double tol, ttn_s** outs, ttn_cbc_report* reps) {
+  CoreCtl sync_cc;
+  const bool part_on = ctx->comm && ctx->parts > 1;
+  if (!ctx->speculate || tol != 0.0 || part_on || nb <= 0 || !ops || !sts || !ops[0] || !sts[0]) {
+    apply_core(ctx, nb, ops, sts, max_bond, tol, outs, reps, sync_cc);
+    return;
+  }
+  for (int b = 0; b < nb; ++b)
+    if (!ops[b] || !sts[b]) throw Error(TTN_ERR_ARG, "NULL handle");
+  auto& G = graphs_of(ctx);
+  const std::vector<int64_t> skey = shape_key(nb, ops, sts, max_bond);
+  // a failed speculation marks the tree (topology, dimensions, max_bond), not just these bonds:
+  // workloads whose ranks are data dependent (circuits) change bonds every apply
+  const std::vector<int64_t> tkey(skey.begin(), skey.begin() + 3 + 2 * sts[0]->n);
+  if (G.failed.count(tkey)) {
+    apply_core(ctx, nb, ops, sts, max_bond, tol, outs, reps, sync_cc);
+    return;
+  }
+  std::vector<int64_t> gkey = skey;
+  for (int b = 0; b < nb; ++b) {
+    gkey.push_back(reinterpret_cast<int64_t>(ops[b]->data));
+    gkey.push_back(reinterpret_cast<int64_t>(sts[b]->data));
+  }
+  if (ctx->graphs) {
+    auto it = G.map.find(gkey);
+    if (it != G.map.end()) {
+      it->second->last_use = ++G.tick;
+      if (replay(ctx, it->second.get(), nb, sts[0], outs, reps)) return;
+      destroy_entry(ctx, it->second.get());
+      G.map.erase(it);
+      G.failed.insert(tkey);
+      apply_core(ctx, nb, ops, sts, max_bond, tol, outs, reps, sync_cc);
+      return;
+    }
+  }
+  // speculative run (uncaptured)
+  const size_t rb = SpecRes::bytes(nb);
+  if (ctx->spec_host_size < rb) {
+    if (ctx->spec_host) cudaFreeHost(ctx->spec_host);
+    ctx->spec_host = nullptr;
+    ctx->spec_host_size = 0;
+    TTN_CUDA(cudaMallocHost(&ctx->spec_host, rb));
+    ctx->spec_host_size = rb;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  CoreCtl cc;
+  cc.mode = Mode::Spec;
+  cc.host_res = ctx->spec_host;
+  ctx->ring->staged = 0;
+  apply_core(ctx, nb, ops, sts, max_bond, tol, outs, nullptr, cc);
+  const size_t staged = ctx->ring->staged;
+  ctx->sync();
+  TTN_CUDA(cudaGetLastError());
+  if (!spec_ok(ctx->spec_host, nb)) {
+    for (int b = 0; b < nb; ++b) {
+      free_ttn(outs[b]);
+      outs[b] = nullptr;
+    }
+    G.failed.insert(tkey);
+    apply_core(ctx, nb, ops, sts, max_bond, tol, outs, reps, sync_cc);
+    return;
+  }
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  fill_reports(reps, nb, ctx->spec_host, cc.flops, cc.maxb, cc.peak, secs, ctx->host_syncs);
+  // capture on the second successful speculative apply of the same key (inputs that are
+  // created afresh for every apply, e.g. from host buffers, never pay for a capture)
+  if (ctx->graphs && !cc.host_synced && !G.nograph.count(gkey) && !G.seen.count(gkey)) {
+    if (G.seen.size() >= 256) G.seen.clear();
+    G.seen.insert(gkey);
+    return;
+  }
+  if (ctx->graphs && !cc.host_synced && !G.nograph.count(gkey)) {
+    G.seen.erase(gkey);
+    std::unique_ptr<GraphEntry> e = capture(ctx, nb, ops, sts, max_bond, staged, cc.out_elems);
+    if (!e) {
+      G.nograph.insert(gkey);
+      return;
+    }
+    e->last_use = ++G.tick;
+    if (G.map.size() >= 8) {   // least recently used entry goes
+      auto old = G.map.begin();
+      for (auto it = G.map.begin(); it != G.map.end(); ++it)
+        if (it->second->last_use < old->second->last_use) old = it;
+      destroy_entry(ctx, old->second.get());
+      G.map.erase(old);
+    }
+    G.map[gkey] = std::move(e);
   }
 }
 

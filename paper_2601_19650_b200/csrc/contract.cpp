@@ -34,6 +34,7 @@ struct PlanT {
   int nin = 0;
   std::vector<StepT> steps;
   double flops = 0.0;
+  double flops_min = 0.0;      // the minimum over all pairwise orders (algorithmic work)
   int64_t peak = 0;
   bool permute_only = false;   // single operand: plain permutation into the output
 };
@@ -133,6 +134,24 @@ PlanT make_plan(const Task& t) {
     const double by = 16.0 * (prod(freel[sa]) + prod(freel[sb]) + prod(freel[sm]));
     return std::max(fl / 37e12, by / 6.5e12) + 2e-7;
   };
+  // algorithmic work: the fewest flops of any pairwise order (what the roofline counts); the
+  // executed order below may spend more flops where that is faster on the device
+  {
+    std::vector<double> fmin(1 << n, 0.0);
+    for (int m = 1; m <= full; ++m) {
+      if ((m & (m - 1)) == 0) continue;
+      fmin[m] = 1e300;
+      for (int sub = (m - 1) & m; sub > 0; sub = (sub - 1) & m) {
+        const int rest = m ^ sub;
+        if (sub < rest) continue;
+        std::vector<int> un = freel[sub];
+        for (int l : freel[rest])
+          if (std::find(un.begin(), un.end(), l) == un.end()) un.push_back(l);
+        fmin[m] = std::min(fmin[m], fmin[sub] + fmin[rest] + 8.0 * prod(un));
+      }
+    }
+    P.flops_min = fmin[full];
+  }
   std::vector<double> best(1 << n, 0.0), peak(1 << n, 0.0);
   std::vector<int> split(1 << n, 0);
   for (int m = 1; m <= full; ++m) {
@@ -382,6 +401,7 @@ void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st) {
     if (!t.out) t.out = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * std::max<int64_t>(tot, 1)));
     st.peak_entries = std::max(st.peak_entries, std::max(tot, plans[i]->peak));
     t.flops = plans[i]->flops;
+    t.flops_min = plans[i]->flops_min;
     max_steps = std::max(max_steps, plans[i]->steps.size());
     if (plans[i]->permute_only) {   // single operand: permutation into the output
       const Operand& o = t.ops[0];

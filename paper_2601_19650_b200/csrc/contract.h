@@ -27,6 +27,7 @@ struct Task {
   int* out_exp = nullptr;              // optional: max binary exponent of the output (GEMM epilogue)
   std::vector<int64_t> out_dims;       // filled by contract_batch
   double flops = 0.0;                  // filled by contract_batch (8 * complex MACs)
+  double flops_min = 0.0;              // filled by contract_batch: the cheapest order's flops
 };
 
 struct ExecStats {

@@ -503,6 +503,168 @@ __device__ void tridiag_stats(const HeevProblem& P, double trace) {
   }
 }
 
+
+// ---------------------------------------------------------------- K0: small Grams (n <= 32)
+// "n <= 64: batched cyclic Jacobi per CTA in shared memory".  One warp per
+// Gram (lane = row), the Hermitian matrix and the eigenvector matrix in shared memory (odd
+// row stride: conflict-free column access), parallel cyclic Jacobi with the round-robin
+// ordering (n/2 disjoint rotations per round, each a complex 2 x 2 Schur rotation
+// U = diag(1, e^{-i phi}) R(c, s)), until the off-diagonal mass is <= (1e-16)^2 ||A||_F^2.
+// Then the descending sort, the truncation decision of heev_finish (k, discarded weight,
+// dropped rows zeroed), the pow2 unscale and the exact-factor skip -- the whole K1..K7
+// pipeline of a small Gram in ONE launch (latency-bound trees: configs 1, 5).
+constexpr int JAC_MAX_N = 32;
+constexpr int JAC_WARPS = 4;
+__host__ __device__ inline int jac_ld(int n) { return n | 1; }
+__host__ __device__ inline size_t jac_warp_bytes(int n) {
+  return (size_t)2 * n * jac_ld(n) * 16 + (size_t)(JAC_MAX_N / 2) * (2 * 4 + 3 * 8) + (size_t)JAC_MAX_N * 12 + 64;
+}
+
+__global__ void __launch_bounds__(JAC_WARPS * 32) heev_jacobi(const HeevProblem* __restrict__ probs, int nprob,
+                                                              int nmax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pi = blockIdx.x * JAC_WARPS + warp;
+  if (pi >= nprob) return;   // whole warp
+  const HeevProblem P = probs[pi];
+  const int n = P.n, kmax = P.kmax, LD = jac_ld(n);
+  if (P.skip && *P.skip) {   // exact-factor shortcut
+    if (lane == 0) {
+      if (P.k_out) *P.k_out = kmax;
+      if (P.w_out) *P.w_out = 0.0;
+    }
+    return;
+  }
+  unsigned char* base = smem_raw + (size_t)warp * jac_warp_bytes(nmax);
+  cplx* A = reinterpret_cast<cplx*>(base);
+  cplx* V = A + (size_t)n * LD;
+  double* rc = reinterpret_cast<double*>(V + (size_t)n * LD);   // per pair: c, s (real), and e^{-i phi}
+  double* rer = rc + JAC_MAX_N / 2 * 2;
+  double* rei = rer + JAC_MAX_N / 2;
+  int* rp = reinterpret_cast<int*>(rei + JAC_MAX_N / 2);
+  int* rq = rp + JAC_MAX_N / 2;
+  double* dsort = reinterpret_cast<double*>(rq + JAC_MAX_N / 2);
+  int* perm = reinterpret_cast<int*>(dsort + JAC_MAX_N);
+  double fro = 0.0, tr = 0.0;
+  for (int e = lane; e < n * n; e += 32) {
+    const int i = e / n, j = e - i * n;
+    const cplx a = P.A[e];
+    A[i * LD + j] = a;
+    V[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    fro += a.x * a.x + a.y * a.y;
+    if (i == j) tr += a.x;
+  }
+  fro = warp_sum(fro);
+  tr = warp_sum(tr);
+  __syncwarp();
+  const int m = n + (n & 1), t = m - 1, np = m / 2;
+  for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
+    double off = 0.0;
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e - i * n;
+      if (i != j) {
+        const cplx a = A[i * LD + j];
+        off += a.x * a.x + a.y * a.y;
+      }
+    }
+    off = warp_sum(off);
+    if (!(off > 1e-32 * fro)) break;
+    for (int r = 0; r < t; ++r) {
+      if (lane < np) {
+        int p, q;
+        if (lane == 0) {
+          p = 0;
+          q = 1 + r % t;
+        } else {
+          p = 1 + (r + lane) % t;
+          q = 1 + (r - lane + t) % t;
+        }
+        double c = 1.0, s = 0.0, er = 1.0, ei = 0.0;
+        if (p < n && q < n) {
+          const cplx apq = A[p * LD + q];
+          const double ar = hypot(apq.x, apq.y);
+          if (ar > 0.0) {
+            const double zeta = (A[q * LD + q].x - A[p * LD + p].x) / (2.0 * ar);
+            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            c = 1.0 / sqrt(1.0 + tt * tt);
+            s = tt * c;
+            er = apq.x / ar;    // e^{-i phi} = conj(apq) / |apq|
+            ei = -apq.y / ar;
+          }
+        }
+        rp[lane] = p;
+        rq[lane] = q;
+        rc[2 * lane] = c;
+        rc[2 * lane + 1] = s;
+        rer[lane] = er;
+        rei[lane] = ei;
+      }
+      __syncwarp();
+      // columns (A U) and the eigenvectors (V U): lane = row
+      for (int i = lane; i < n; i += 32)
+        for (int k = 0; k < np; ++k) {
+          const int p = rp[k], q = rq[k];
+          if (p >= n || q >= n) continue;
+          const double c = rc[2 * k], s = rc[2 * k + 1], er = rer[k], ei = rei[k];
+          for (int w = 0; w < 2; ++w) {
+            cplx* M = w ? V : A;
+            const cplx x = M[i * LD + p], y = M[i * LD + q];
+            const cplx ey = make_double2(er * y.x - ei * y.y, er * y.y + ei * y.x);   // e^{-i phi} y
+            M[i * LD + p] = make_double2(c * x.x - s * ey.x, c * x.y - s * ey.y);
+            M[i * LD + q] = make_double2(s * x.x + c * ey.x, s * x.y + c * ey.y);
+          }
+        }
+      __syncwarp();
+      // rows (U^H A): lane = column
+      for (int j = lane; j < n; j += 32)
+        for (int k = 0; k < np; ++k) {
+          const int p = rp[k], q = rq[k];
+          if (p >= n || q >= n) continue;
+          const double c = rc[2 * k], s = rc[2 * k + 1], er = rer[k], ei = -rei[k];   // e^{+i phi}
+          const cplx x = A[p * LD + j], y = A[q * LD + j];
+          const cplx ey = make_double2(er * y.x - ei * y.y, er * y.y + ei * y.x);
+          A[p * LD + j] = make_double2(c * x.x - s * ey.x, c * x.y - s * ey.y);
+          A[q * LD + j] = make_double2(s * x.x + c * ey.x, s * x.y + c * ey.y);
+        }
+      __syncwarp();
+    }
+  }
+  // descending order (ties by index)
+  for (int i = lane; i < n; i += 32) dsort[i] = A[i * LD + i].x;
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    const double di = dsort[i];
+    int rk = 0;
+    for (int j = 0; j < n; ++j) rk += (dsort[j] > di || (dsort[j] == di && j < i)) ? 1 : 0;
+    perm[rk] = i;
+  }
+  __syncwarp();
+  // truncation decision (heev_finish semantics)
+  const double l1 = dsort[perm[0]];
+  int k = 1;
+  double kept = 0.0;
+  const bool zero = !(tr > 0.0 && l1 > 0.0);
+  if (!zero) {
+    int cnt = 0;
+    for (int u = 0; u < kmax; ++u) {
+      const double lu = dsort[perm[u]];
+      if (lu > P.tol2 * l1 && lu > P.floor_rel * l1) ++cnt;
+    }
+    k = cnt < 1 ? 1 : (cnt > P.max_bond ? P.max_bond : cnt);
+    for (int u = 0; u < k; ++u) kept += dsort[perm[u]];
+  }
+  const int e2 = P.exp2 ? pow2_effective(*P.exp2) : 0;
+  for (int u = lane; u < kmax; u += 32) P.lam[u] = (!zero && u < k) ? ldexp(dsort[perm[u]], 2 * e2) : 0.0;
+  for (int e = lane; e < kmax * n; e += 32) {
+    const int u = e / n, i = e - u * n;
+    P.Vt[e] = (zero || u < k) ? V[i * LD + perm[u]] : make_double2(0.0, 0.0);
+  }
+  if (lane == 0) {
+    if (P.k_out) *P.k_out = k;
+    if (P.w_out) *P.w_out = ldexp(fmax(tr - kept, 0.0), 2 * e2);
+  }
+}
+
 // ---------------------------------------------------------------- K1: tridiagonalisation
 template <int NQ>
 __global__ void __launch_bounds__(HEEV_THREADS, NQ == 4 ? 3 : 2) heev_tridiag(const HeevProblem* __restrict__ probs) {
@@ -1565,9 +1727,31 @@ void launch_tridiag_cluster(const HeevProblem* d, int nprob, int cs, size_t smem
 }
 }  // namespace
 
-void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s, const std::function<void()>& values_ready) {
+void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const std::function<void()>& values_ready) {
   HostScope hs_("launch_heev");
-  if (n == 0) return;
+  if (nin == 0) return;
+  // K0: Grams of order <= 32 in one launch (warp per Gram); the rest take K1..K7
+  std::vector<HeevProblem> small, rest;
+  for (int i = 0; i < nin; ++i) (hin[i].n <= JAC_MAX_N ? small : rest).push_back(hin[i]);
+  if (!small.empty()) {
+    int nmax = 1;
+    for (auto& p : small) nmax = std::max(nmax, p.n);
+    const size_t sm = jac_warp_bytes(nmax) * JAC_WARPS;
+    func_smem(heev_jacobi, jac_warp_bytes(JAC_MAX_N) * JAC_WARPS);
+    const HeevProblem* dj = static_cast<const HeevProblem*>(st.put(small.data(), sizeof(HeevProblem) * small.size()));
+    double fl = 0.0;
+    for (auto& p : small) fl += 8.0 * 8.0 * (double)p.n * p.n * p.n;   // ~8 sweeps of 8 n^3 flops
+    prof_begin(s);
+    heev_jacobi<<<((int)small.size() + JAC_WARPS - 1) / JAC_WARPS, JAC_WARPS * 32, sm, s>>>(dj, (int)small.size(), nmax);
+    prof_end(s, "heev", fl, 32.0 * (double)small.size());
+    count_launch();
+  }
+  if (rest.empty()) {
+    if (values_ready) values_ready();
+    return;
+  }
+  HeevProblem* h = rest.data();
+  const int n = (int)rest.size();
   func_smem(heev_tridiag<4>, FUSED_SMEM_BUDGET);
   func_smem(heev_tridiag<6>, FUSED_SMEM_BUDGET);
   func_smem(heev_tridiag<8>, FUSED_SMEM_BUDGET);

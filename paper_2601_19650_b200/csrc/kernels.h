@@ -163,6 +163,7 @@ struct Stager {
     return tmp_.data();
   }
   virtual void* commit(void* host, size_t bytes) { return put(host, bytes); }
+  virtual void epoch() {}   // after a full stream synchronisation
   virtual ~Stager() {}
  private:
   std::vector<char> tmp_;
@@ -215,8 +216,17 @@ inline void func_smem(F* func, size_t bytes) {
   func_attr(reinterpret_cast<const void*>(func), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// Speculative ranks (cbc.cpp): the host plans with k = kmax and checks on the device.
+// One thread per compress: flag |= 1 if the eigensolver's rank differs from kmax, |= 2 if the
+// discarded weight is not finite; wacc[inst] += w, xacc[inst] += skip (exact-factor count).
+struct SpecCheck { const int* k; const double* w; const int* skip; int kmax; int inst; };
+void launch_spec_check(SpecCheck* h, int n, double* wacc, int* xacc, int* flag, Stager& st, cudaStream_t s);
+// flag |= bit if any of info[0..n) is non-zero (CholeskyQR pivot failures)
+void launch_flag_nonzero(const int* info, int n, int* flag, int bit, cudaStream_t s);
+
 // Counters of kernel launches issued by this library (for the bench's gpu_launches claim).
 long long launch_count();
 void count_launch();
+void add_launches(long long delta);   // graph replays (+ nodes) and captures (- recorded launches)
 
 }  // namespace tcbc

@@ -17,6 +17,7 @@ namespace tcbc {
 static std::atomic<long long> g_launches{0};
 long long launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
+void add_launches(long long delta) { g_launches.fetch_add(delta); }
 
 void func_attr(const void* func, cudaFuncAttribute attr, int value) {
   static std::mutex mu;
@@ -138,7 +139,38 @@ __global__ void pow2_scale(const Pow2Problem* __restrict__ probs, int sign) {
   }
 }
 
+__global__ void spec_check(const SpecCheck* __restrict__ p, int n, double* wacc, int* xacc, int* flag) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const SpecCheck c = p[j];
+  const double w = *c.w;
+  int f = 0;
+  if (*c.k != c.kmax) f |= 1;
+  if (!isfinite(w)) f |= 2;
+  if (f) atomicOr(flag, f);
+  atomicAdd(wacc + c.inst, w);
+  if (c.skip && *c.skip) atomicAdd(xacc + c.inst, 1);
+}
+
+__global__ void flag_nonzero(const int* info, int n, int* flag, int bit) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n && info[j] != 0) atomicOr(flag, bit);
+}
+
 }  // namespace
+
+void launch_spec_check(SpecCheck* h, int n, double* wacc, int* xacc, int* flag, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  const SpecCheck* d = static_cast<const SpecCheck*>(st.put(h, sizeof(SpecCheck) * n));
+  spec_check<<<(n + 127) / 128, 128, 0, s>>>(d, n, wacc, xacc, flag);
+  count_launch();
+}
+
+void launch_flag_nonzero(const int* info, int n, int* flag, int bit, cudaStream_t s) {
+  if (n == 0) return;
+  flag_nonzero<<<(n + 127) / 128, 128, 0, s>>>(info, n, flag, bit);
+  count_launch();
+}
 
 void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s) {
   long long total = 0;

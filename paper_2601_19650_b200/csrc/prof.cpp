@@ -16,6 +16,7 @@ struct Pending {
   cudaEvent_t a, b;
   std::string family;
   double flops, bytes;
+  bool owned = false;   // events belong to a graph (ProfSink): not returned to the pool
 };
 
 struct Acc {
@@ -60,8 +61,10 @@ struct Profiler {
       t.flops += p.flops;
       t.bytes += p.bytes;
       t.launches += 1;
-      pool.push_back(p.a);
-      pool.push_back(p.b);
+      if (!p.owned) {
+        pool.push_back(p.a);
+        pool.push_back(p.b);
+      }
     }
     pending.clear();
   }
@@ -74,12 +77,32 @@ Profiler& P() {
 
 thread_local cudaEvent_t t_open = nullptr;   // per host thread (worker contexts run concurrently)
 thread_local cudaEvent_t t_gap = nullptr;    // recorded right after a host synchronisation
+thread_local ProfSink* t_sink = nullptr;     // graph capture in progress on this thread
 
 }  // namespace
 
+ProfSink::~ProfSink() {
+  for (auto& r : recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+}
+
+void prof_set_sink(ProfSink* s) { t_sink = s; }
+
+bool prof_on() { return P().on; }
+
+void prof_replay(const ProfSink& s) {
+  Profiler& p = P();
+  if (!p.on || s.recs.empty()) return;
+  std::lock_guard<std::mutex> g(p.mu);
+  for (auto& r : s.recs) p.pending.push_back(Pending{r.a, r.b, r.family, r.flops, r.bytes, true});
+  p.harvest();   // the next replay re-records these events: read them now (the caller synchronised)
+}
+
 void prof_mark_sync(cudaStream_t s) {
   Profiler& p = P();
-  if (!p.on) return;
+  if (!p.on || t_sink) return;
   std::lock_guard<std::mutex> g(p.mu);
   if (t_gap) p.pool.push_back(t_gap);
   t_gap = p.get();
@@ -89,6 +112,13 @@ void prof_mark_sync(cudaStream_t s) {
 void prof_begin(cudaStream_t s) {
   Profiler& p = P();
   if (!p.on) return;
+  if (t_sink) {   // capture: a fresh event owned by the graph
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    t_open = e;
+    return;
+  }
   std::lock_guard<std::mutex> g(p.mu);
   if (t_gap) {   // device idle from the synchronisation to this launch set: host work in between
     cudaEvent_t e = p.get();
@@ -103,6 +133,15 @@ void prof_begin(cudaStream_t s) {
 void prof_end(cudaStream_t s, const char* family, double flops, double bytes) {
   Profiler& p = P();
   if (!p.on) return;
+  if (t_sink) {
+    if (!t_open) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, s);
+    t_sink->recs.push_back(ProfSink::Rec{t_open, b, family, flops, bytes});
+    t_open = nullptr;
+    return;
+  }
   std::lock_guard<std::mutex> g(p.mu);
   if (!t_open) return;
   cudaEvent_t b = p.get();

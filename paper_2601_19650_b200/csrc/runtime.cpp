@@ -25,6 +25,7 @@ void* Arena::alloc(size_t bytes) {
     ++cur_;
   }
   size_t sz = std::max(bytes, chunk_);
+  if (frozen) throw Error(TTN_ERR_UNSUPPORTED, "arena growth during a graph capture");
   char* p = nullptr;
   if (src_) {
     p = static_cast<char*>(src_->get(sz));
@@ -79,6 +80,7 @@ void* RingStager::put(const void* host, size_t bytes) {
   TTN_CUDA(cudaMemcpyAsync(d_ + off_, h_ + off_, bytes, cudaMemcpyHostToDevice, s_));
   void* d = d_ + off_;
   off_ += b;
+  staged += b;
   return d;
 }
 
@@ -98,8 +100,24 @@ void* RingStager::commit(void* host, size_t bytes) {
   TTN_CUDA(cudaMemcpyAsync(d_ + off_, h, bytes, cudaMemcpyHostToDevice, s_));
   void* d = d_ + off_;
   off_ += (bytes + 255) & ~size_t(255);
+  staged += (bytes + 255) & ~size_t(255);
   return d;
 }
+
+void* CaptureStager::put(const void* host, size_t bytes) {
+  const size_t off = shadow.size(), b = (bytes + 255) & ~size_t(255);
+  if (off + b > cap_) throw Error(TTN_ERR_UNSUPPORTED, "graph descriptor buffer too small");
+  shadow.resize(off + b);
+  std::memcpy(shadow.data() + off, host, bytes);
+  return d_ + off;
+}
+
+void* CaptureStager::reserve(size_t bytes) {
+  tmp_.resize(bytes);
+  return tmp_.data();
+}
+
+void* CaptureStager::commit(void* host, size_t bytes) { return put(host, bytes); }
 
 void RingStager::epoch() { off_ = 0; }
 
@@ -151,7 +169,8 @@ void finalize_shapes(ttn_s* t) {
   t->total = off;
 }
 
-ttn_s* new_ttn_like(ttn_ctx_s* ctx, const ttn_s* tmpl, int kind, const std::vector<int64_t>& bond) {
+ttn_s* new_ttn_like(ttn_ctx_s* ctx, const ttn_s* tmpl, int kind, const std::vector<int64_t>& bond,
+                    const std::function<cplx*(int64_t)>& alloc) {
   ttn_s* t = new ttn_s();
   t->ctx = ctx;
   t->kind = kind;
@@ -165,7 +184,7 @@ ttn_s* new_ttn_like(ttn_ctx_s* ctx, const ttn_s* tmpl, int kind, const std::vect
   t->bond[t->root] = 1;
   finalize_shapes(t);
   try {
-    t->data = static_cast<cplx*>(ctx->get(sizeof(cplx) * std::max<int64_t>(t->total, 1)));
+    t->data = alloc ? alloc(t->total) : static_cast<cplx*>(ctx->get(sizeof(cplx) * std::max<int64_t>(t->total, 1)));
   } catch (...) {
     delete t;
     throw;

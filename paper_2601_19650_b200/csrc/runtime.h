@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -42,6 +43,7 @@ class Arena {
   explicit Arena(size_t chunk = 256ull << 20) : chunk_(chunk) {}
   ~Arena();
   void set_source(MemSource* src) { src_ = src; }
+  bool frozen = false;   // set during a graph capture: a new chunk would escape the graph
   void* alloc(size_t bytes);
   void reset();
   void release();
@@ -62,7 +64,8 @@ class RingStager : public Stager {
   void* put(const void* host, size_t bytes) override;
   void* reserve(size_t bytes) override;
   void* commit(void* host, size_t bytes) override;
-  void epoch();   // call after a stream synchronisation: the whole ring is free again
+  void epoch() override;   // call after a stream synchronisation: the whole ring is free again
+  size_t staged = 0;       // bytes staged since the last reset (the size a capture needs)
  private:
   cudaStream_t s_;
   char* h_ = nullptr;
@@ -70,12 +73,38 @@ class RingStager : public Stager {
   size_t size_, off_ = 0;
 };
 
+// Stager of a CUDA-graph capture: descriptors are written to a host shadow at the offsets
+// they will have in a device buffer owned by the graph (addresses known while capturing);
+// the shadow is uploaded once after the capture ends.  Never copies or synchronises.
+class CaptureStager : public Stager {
+ public:
+  CaptureStager(char* dev, size_t cap) : d_(dev), cap_(cap) {}
+  void* put(const void* host, size_t bytes) override;
+  void* reserve(size_t bytes) override;
+  void* commit(void* host, size_t bytes) override;
+  std::vector<char> shadow;
+ private:
+  char* d_;
+  size_t cap_;
+  std::vector<char> tmp_;
+};
+
 }  // namespace tcbc
+
+namespace tcbc { struct GraphCache; }
 
 struct ttn_ctx_s : tcbc::MemSource {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string last_error;
+  // level-synchronous schedule options (ttn_ctx_set_schedule): speculative ranks (no host
+  // synchronisation inside an apply) and CUDA-graph replay of speculative applies
+  bool speculate = true;
+  bool graphs = true;
+  bool capturing = false;        // a graph capture is in progress on this ctx (no arena growth)
+  tcbc::GraphCache* gr = nullptr;          // graph cache and the shapes whose speculation failed
+  char* spec_host = nullptr;     // pinned result block of a speculative apply
+  size_t spec_host_size = 0;
   // device memory: the caller's allocator (ttn_ctx_create), else `pool` (owned by the root
   // context; worker contexts share it).  Frees through a caller's allocator are deferred until
   // the ctx stream has passed an event recorded at the free, so the allocator may hand the
@@ -88,7 +117,8 @@ struct ttn_ctx_s : tcbc::MemSource {
   void* get(size_t bytes) override;
   void put(void* p) override;
   void reap(bool all);   // hand completed deferred frees to the caller's allocator
-  tcbc::RingStager* stager = nullptr;
+  tcbc::RingStager* ring = nullptr;   // the descriptor ring (owned)
+  tcbc::Stager* stager = nullptr;     // current stager: the ring, or a capture's
   tcbc::Arena scratch;      // per-stage temporaries (reset between stages)
   tcbc::Arena env;          // per-apply environment factors (reset per apply)
   // pinned host buffer for small D2H reads (ranks, weights, norms)
@@ -132,12 +162,15 @@ namespace tcbc {
 // Topology helpers shared by create / apply / overlap.
 void build_topology(ttn_s* t, const int32_t* parent, int n);
 void finalize_shapes(ttn_s* t);   // shapes / offsets / total from kind, phys, bond
-ttn_s* new_ttn_like(ttn_ctx_s* ctx, const ttn_s* tmpl, int kind, const std::vector<int64_t>& bond);
+// data from `alloc` when given (a graph capture's output buffer), else from the ctx
+ttn_s* new_ttn_like(ttn_ctx_s* ctx, const ttn_s* tmpl, int kind, const std::vector<int64_t>& bond,
+                    const std::function<cplx*(int64_t)>& alloc = std::function<cplx*(int64_t)>());
 void free_ttn(ttn_s* t);
 
 // Batched drivers (cbc.cpp)
 void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* const* sts,
                     int64_t max_bond, double tol, ttn_s** outs, ttn_cbc_report* reps);
+void graphs_release(ttn_ctx_s* ctx);   // before the ctx's arenas / pool go
 void overlap_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* a, const ttn_s* const* b, cplx* out);
 // One layer of a <bra| O_1 ... O_m |ket> sweep (per-instance handles).
 struct SweepLayer {
