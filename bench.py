@@ -340,12 +340,10 @@ def run_native(args, rank, world, local_rank):
         reps = last["reps"]
         return sum(r["flops_gemm_min"] for r in reps), sum(r["flops_gemm_exec"] for r in reps)
 
-    # FP64-bound configs (3, 4) time their kernels inside the timed region (CUDA events on the
-    # library stream; graphs captured during the warm-up carry the event nodes); the
-    # latency-bound ones (1, 2, 5) are timed without events and profiled in a separate pass
-    prof_in_loop = cfg in (3, 4)
-    if prof_in_loop:
-        P.ttn_profile_enable(True)
+    # The timed region replays CUDA graphs (speculative schedule, ttn_ctx_set_schedule), which
+    # carry no per-launch events; the kernel-family times (roofline) come from a profiled pass
+    # of the same steps right after it: speculative schedule without graphs, CUDA events on the
+    # library stream around every launch set.
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -355,7 +353,6 @@ def run_native(args, rank, world, local_rank):
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         clocks.start()
         time.sleep(0.3)
-    P.ttn_profile_enable(prof_in_loop)
     lc0 = P.ttn_launch_count()
     if world > 1:
         dist.barrier()
@@ -378,15 +375,23 @@ def run_native(args, rank, world, local_rank):
         dist.barrier()
     launches = P.ttn_launch_count() - lc0
     clk = clocks.stop(local_rank) if clocks else None
-    prof_steps = args.steps
-    if not prof_in_loop:   # separate profiled pass, graphs off so the events bracket each launch set
-        prof_steps = min(args.steps, 5)
-        P.ttn_ctx_set_schedule(ctx, True, False)
-        P.ttn_profile_enable(True)
-        for _ in range(prof_steps):
-            step()
-        torch.cuda.synchronize()
-        P.ttn_ctx_set_schedule(ctx, True, True)
+    # profiled pass: graphs off so the events bracket each launch set
+    prof_steps = args.steps if cfg in (3, 4) else min(args.steps, 5)
+    P.ttn_ctx_set_schedule(ctx, True, False)
+    step()                                   # (re-plans without graphs; untimed)
+    torch.cuda.synchronize()
+    P.ttn_profile_enable(True)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    p_applies = 0
+    for _ in range(prof_steps):
+        if flush is not None:
+            flush.zero_()
+        p_applies += step()[0]
+    pe1.record(stream)
+    pe1.synchronize()
+    prof_ms = pe0.elapsed_time(pe1)
+    P.ttn_ctx_set_schedule(ctx, True, True)
     prof = {fam: P.ttn_profile_read(fam) for fam in ("all", "zgemm", "heev", "heev_large", "potrf", "trtri", "geqr", "permute",
                                                      "scale_rows", "misc", "gap_after_sync")}
     P.ttn_profile_enable(False)
@@ -539,8 +544,10 @@ def run_native(args, rank, world, local_rank):
                      "peak_source": FP64_PEAK_SOURCE,
                      "flops": "algorithmic: node contractions at their cheapest pairwise order, Grams as HERK "
                               "(4 n^2 K), factor / S / CholeskyQR / R products (ttn_cbc_report.flops_gemm_min); "
-                              "zgemm time = CUDA events " + ("in the timed region" if prof_in_loop else
-                                                             f"of a separate profiled pass ({prof_steps} steps)"),
+                              f"zgemm time = CUDA events around every launch set in a profiled pass of {prof_steps} "
+                              "steps right after the timed region (speculative schedule without graphs)",
+                     "profiled_pass": {"steps": prof_steps, "ms_per_step": prof_ms / prof_steps,
+                                       "applies_per_s": p_applies / (prof_ms / 1000.0)},
                      "algorithmic_flops_per_step": gmin,
                      "kernel_efficiency": {"achieved": ach_exec, "frac": ach_exec / FP64_PEAK_TFLOPS,
                                            "executed_flops_per_step": gexec,

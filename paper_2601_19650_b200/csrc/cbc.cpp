@@ -135,10 +135,15 @@ void check_heev_size(int64_t nn) {
 // Gram -> eigenpairs -> factor, for every job; synchronises once to read the ranks.
 void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_bond, double tol,
                     ExecStats& st, std::vector<double>& w_inst, std::vector<FlopAcc>& flops_inst,
-                    std::vector<int>& exact_inst, const SpecDev* spec) {
+                    std::vector<int>& exact_inst, const SpecDev* spec, Comm* shard = nullptr) {
   if (jobs.empty()) return;
   HostScope hs_("compress_batch");
   const int nj = (int)jobs.size();
+  // sharded (replicated top of a partitioned apply): job j's Gram, eigensolve and
+  // factor run on rank j % world only; the factor rows, rank, discarded weight and shortcut
+  // flag are then broadcast from that rank
+  const bool sharded = shard && shard->world > 1 && !spec;
+  auto mine = [&](int j) { return !sharded || j % shard->world == shard->rank; };
   std::vector<GemmProblem> grams, fgemm;
   std::vector<HeevProblem> hp(nj);
   std::vector<ScaleRowsProblem> sr;
@@ -154,8 +159,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   int* d_cinfo = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nj));
   TTN_CUDA(cudaMemsetAsync(d_skip, 0, sizeof(int) * nj, ctx->stream));
   std::vector<PermProblem> ccopy;
-  std::vector<PotrfProblem> cpot;
-  std::vector<TrtriProblem> ctri;
+  std::vector<PotriProblem> cpot;
   std::vector<CertProblem> ccert;
   std::vector<ExactFactorProblem> cfac;
   for (int j = 0; j < nj; ++j) {
@@ -170,7 +174,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       GemmProblem g = (m >= n) ? mk_gemm(J.X, OP_C, n, J.X, OP_N, n, G, nn, n, n, m)     // G = X^H X
                                : mk_gemm(J.X, OP_N, n, J.X, OP_C, n, G, nn, m, m, n);    // K = X X^H
       g.sym = 1;   // Hermitian: lower tiles + mirror (HERK)
-      grams.push_back(g);
+      if (mine(j)) grams.push_back(g);
       flops_inst[J.inst] += gemm_flops(g);
     } else if (m < n) {
       throw Error(TTN_ERR_ARG, "row-split compress needs the G route (m >= n)");
@@ -199,20 +203,20 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
     if (m >= n) {
       ScaleRowsProblem s{};
       s.Vt = h.Vt; s.lam = h.lam; s.F = J.dst->p; s.kmax = (int)kmax; s.n = (int)n;
-      sr.push_back(s);
+      if (mine(j)) sr.push_back(s);
     } else {   // F = conj(Vt) X  (U_k^H X)
-      fgemm.push_back(mk_gemm(h.Vt, OP_R, m, J.X, OP_N, n, J.dst->p, n, kmax, n, m));
+      if (mine(j)) fgemm.push_back(mk_gemm(h.Vt, OP_R, m, J.X, OP_N, n, J.dst->p, n, kmax, n, m));
       flops_inst[J.inst] += 8.0 * (double)kmax * n * m;
     }
     st.peak_entries = std::max(st.peak_entries, nn * nn);
-    if (tol == 0.0 && kmax == nn && !chfsi_applicable((int)nn, (int)kmax) && (m >= n || J.X)) {
+    // (Grams of order <= heev_small_n() take the one-launch Jacobi solver: nothing to save)
+    if (mine(j) && tol == 0.0 && kmax == nn && nn > heev_small_n() && !chfsi_applicable((int)nn, (int)kmax) && (m >= n || J.X)) {
       cplx* Wc = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
       cplx* Li = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
       PermProblem pp{};
       pp.src = G; pp.dst = Wc; pp.rank = 1; pp.dims[0] = nn * nn; pp.sstride[0] = 1; pp.total = nn * nn;
       ccopy.push_back(pp);
-      cpot.push_back(PotrfProblem{Wc, nn, (int)nn, 0, d_cinfo + j, 0.0, 0.0});
-      ctri.push_back(TrtriProblem{Wc, Li, nn, (int)nn, 0});
+      cpot.push_back(PotriProblem{Wc, nn, (int)nn, 1, d_cinfo + j, 0.0, 0.0, Li});
       ccert.push_back(CertProblem{G, Li, d_cinfo + j, d_skip + j, (int)nn, 0, kExactCert});
       h.skip = d_skip + j;
       ExactFactorProblem ef{};
@@ -229,7 +233,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   {   // the Gram squares X: exponents from the producing GEMM's epilogue where available
     std::vector<Pow2Problem> have, need, back;
     for (int j = 0; j < nj; ++j) {
-      if (jobs[j].G_pre) continue;   // row-split: X was scaled before its partial Grams
+      if (jobs[j].G_pre || !mine(j)) continue;   // row-split: X was scaled before its partial Grams
       (jobs[j].exp ? have : need).push_back(p2[j]);
       back.push_back(p2[j]);
     }
@@ -240,8 +244,7 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   }
   if (!ccert.empty()) {   // exact-factor shortcut: Cholesky of a copy of each candidate's Gram
     launch_permute(ccopy.data(), (int)ccopy.size(), *ctx->stager, ctx->stream);
-    launch_potrf(cpot.data(), (int)cpot.size(), *ctx->stager, ctx->stream);
-    launch_trtri(ctri.data(), (int)ctri.size(), *ctx->stager, ctx->stream);
+    launch_potri(cpot.data(), (int)cpot.size(), *ctx->stager, ctx->stream);
     launch_chol_certify(ccert.data(), (int)ccert.size(), *ctx->stager, ctx->stream);
   }
   if (spec) {   // speculative: k = kmax, checked on the device (no host read, no sync)
@@ -287,23 +290,37 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
   {   // small Grams: tridiagonal pipeline (heev.cu); large ones: Chebyshev subspace (chfsi.cu)
     std::vector<HeevProblem> small;
     std::vector<HeevProblem*> large;
-    for (auto& h : hp) {
+    for (int j = 0; j < nj; ++j) {
+      if (!mine(j)) continue;
+      HeevProblem& h = hp[j];
       if (chfsi_applicable(h.n, h.kmax)) large.push_back(&h);
       else small.push_back(h);
     }
     std::function<void()> ready;
-    if (large.empty())
+    if (large.empty() && !sharded)
       ready = [&]() {
         read_ranks();
         ctx->mark_ranks();
         early = true;
       };
     if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream, ready);
+    else if (ready) ready();
     chfsi_heev(ctx, large, st);
   }
   if (!sr.empty()) launch_scale_rows(sr.data(), (int)sr.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, fgemm, st);
   launch_exact_factor(cfac.data(), (int)cfac.size(), *ctx->stager, ctx->stream);   // certified jobs
+  if (sharded) {   // results from each job's rank
+    shard->group_start();
+    for (int j = 0; j < nj; ++j) {
+      const int owner = j % shard->world;
+      shard->bcast(jobs[j].dst->p, sizeof(cplx) * kmaxs[j] * jobs[j].n, owner, ctx->stream);
+      shard->bcast(d_k + j, sizeof(int), owner, ctx->stream);
+      shard->bcast(d_w + j, sizeof(double), owner, ctx->stream);
+      shard->bcast(d_skip + j, sizeof(int), owner, ctx->stream);
+    }
+    shard->group_end();
+  }
   if (early) {
     ctx->wait_ranks();
   } else {
@@ -331,8 +348,7 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
   HostScope hs_("qr_batch");
   std::vector<EyeProblem> eyes;
   std::vector<GemmProblem> g1, g2, g3, g4;
-  std::vector<PotrfProblem> p1, p2;
-  std::vector<TrtriProblem> t1, t2;
+  std::vector<PotriProblem> p1, p2;
   std::vector<int> tall;
   int* d_info = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * 2 * jobs.size()));
   TTN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int) * 2 * jobs.size(), ctx->stream));   // Q = I jobs stay 0
@@ -357,13 +373,11 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
     };
     g1.push_back(gp(J.S, OP_C, k, J.S, OP_N, k, W, k, k, m));        // W = S^H S
     g1.back().sym = 1;
-    p1.push_back(PotrfProblem{W, k, (int)k, 0, d_info + 2 * j, kCholTol});
-    t1.push_back(TrtriProblem{W, Li, k, (int)k, 0});
+    p1.push_back(PotriProblem{W, k, (int)k, 0, d_info + 2 * j, kCholTol, 0.0, Li});
     g2.push_back(gp(J.S, OP_N, k, Li, OP_C, k, Q1, m, k, k));        // Q1 = S L^{-H}
     g3.push_back(gp(Q1, OP_C, k, Q1, OP_N, k, W2, k, k, m));         // W2 = Q1^H Q1
     g3.back().sym = 1;
-    p2.push_back(PotrfProblem{W2, k, (int)k, 0, d_info + 2 * j + 1, kCholTol * 1e-2});
-    t2.push_back(TrtriProblem{W2, Li2, k, (int)k, 0});
+    p2.push_back(PotriProblem{W2, k, (int)k, 0, d_info + 2 * j + 1, kCholTol * 1e-2, 0.0, Li2});
     g4.push_back(gp(Q1, OP_N, k, Li2, OP_C, k, J.Q, m, k, k));       // Q = Q1 L2^{-H}
     flops_inst[J.inst].add_nongemm(8.0 * 2.0 * (k * k * k / 3.0));
   }
@@ -381,12 +395,10 @@ int qr_batch(ttn_ctx_s* ctx, std::vector<QRJob>& jobs, ExecStats& st, std::vecto
     launch_pow2_normalize(need.data(), (int)need.size(), *ctx->stager, ctx->stream);
   }
   gemm_batch(ctx, g1, st);
-  launch_potrf(p1.data(), (int)p1.size(), *ctx->stager, ctx->stream);
-  launch_trtri(t1.data(), (int)t1.size(), *ctx->stager, ctx->stream);
+  launch_potri(p1.data(), (int)p1.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, g2, st);
   gemm_batch(ctx, g3, st);
-  launch_potrf(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
-  launch_trtri(t2.data(), (int)t2.size(), *ctx->stager, ctx->stream);
+  launch_potri(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
   gemm_batch(ctx, g4, st);
   if (spec) {   // speculative: a pivot failure (rank-deficient S) invalidates the apply
     launch_flag_nonzero(d_info, 2 * (int)jobs.size(), spec->flag, 4, ctx->stream);
@@ -671,7 +683,7 @@ void apply_core(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* co
       sp_j[q].exp = d_e + q;
       sp_j[q].X = nullptr;
     }
-    compress_batch(ctx, sp_j, max_bond, tol, st, w_inst, flops_inst, exact_inst, spec);
+    compress_batch(ctx, sp_j, max_bond, tol, st, w_inst, flops_inst, exact_inst, spec, comm);
   };
 
   // ---------------- 1. up-sweep (Eq. 10) over the nodes selected by `sel`, deepest level first
@@ -710,7 +722,8 @@ void apply_core(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* co
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
       for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst].add_contract(tasks[j].flops, tasks[j].flops_min);
       st.flops += cs.flops;
-      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub), spec);
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub), spec,
+                     sub ? nullptr : comm);   // the replicated top's compresses: sharded
       ctx->scratch.reset();
     }
   };
@@ -754,7 +767,8 @@ void apply_core(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* co
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
       for (size_t j = 0; j < jobs.size(); ++j) acc_f(sub)[jobs[j].inst].add_contract(tasks[j].flops, tasks[j].flops_min);
       st.flops += cs.flops;
-      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub), spec);
+      compress_batch(ctx, jobs, max_bond, tol, st, acc_w(sub), acc_f(sub), acc_x(sub), spec,
+                     sub ? nullptr : comm);   // the replicated top's compresses: sharded
       ctx->scratch.reset();
     }
   };
@@ -838,6 +852,162 @@ void apply_core(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* co
     cc.out_elems += outs[b]->total;
   }
 
+  // ---------------- row split of the replicated top's heavy final-sweep nodes (partitioned
+  // apply, SURVEY §8(e) "Junction CholeskyQR2 row-split"): Z_i is cut along its widest child
+  // factor leg into slices (rank r contracts slices s = r mod world); then, with the partial
+  // sums all-reduced over the ranks,
+  //   S_s = Z_s L^T,  W = sum_s S_s^H S_s = L1 L1^H,  Q1_s = S_s L1^-H,
+  //   W2 = sum_s Q1_s^H Q1_s = L2 L2^H,  Q_s = Q1_s L2^-H          (CholeskyQR2, Eq. 13)
+  //   R_i = sum_s Q_s^H Z_s                                          (Eq. 14 with Q*)
+  // and every rank scatters its slices' rows of Q into the (zeroed) new tensor T'_i, which an
+  // all-reduce completes on every rank.  Exact up to the order of the row sums.
+  auto final_split = [&](int b, int i, const Task& t) {
+    HostScope hs_("final_split");
+    const Fac& fd = down[(size_t)b * n + i];
+    const int64_t nz = fd.a * fd.b, kd = fd.k, r = rb[b][i], d = ref->phys[i];
+    size_t fo = 2;   // the widest child factor
+    for (size_t o = 3; o < t.ops.size(); ++o)
+      if (t.ops[o].dims[0] > t.ops[fo].dims[0]) fo = o;
+    const int cpos = (int)fo - 2;   // child position of the sliced leg
+    const int64_t kfull = t.ops[fo].dims[0];
+    std::vector<int64_t> rc;        // child factor ranks (leg order)
+    for (size_t o = 2; o < t.ops.size(); ++o) rc.push_back(t.ops[o].dims[0]);
+    int64_t ms = d;
+    for (auto x : rc) ms *= x;
+    std::vector<Task> sl;
+    std::vector<int64_t> k0s, k1s;
+    for (int s = 0; s < nslices; ++s) {
+      if (s % part.world != part.rank) continue;
+      const int64_t k0 = kfull * s / nslices, k1 = kfull * (s + 1) / nslices;
+      if (k1 <= k0) continue;
+      Task ts = t;
+      ts.ops[fo].ptr += k0 * ts.ops[fo].dims[1] * ts.ops[fo].dims[2];
+      ts.ops[fo].dims[0] = k1 - k0;
+      ts.out = nullptr;
+      sl.push_back(ts);
+      k0s.push_back(k0);
+      k1s.push_back(k1);
+    }
+    const int nsl = (int)sl.size();
+    ExecStats cs;
+    if (nsl) contract_batch(ctx, sl, cs);
+    st.peak_entries = std::max(st.peak_entries, cs.peak_entries);
+    for (auto& x : sl) flops_sub[b].add_contract(x.flops, x.flops_min);
+    int* d_e = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * 2 + sizeof(int) * 2));
+    int* d_info = d_e + 2;
+    pow2_reset(d_e, 1, ctx->stream);
+    std::vector<cplx*> S(nsl), Q1(nsl), Q(nsl);
+    std::vector<int64_t> mss(nsl);
+    std::vector<GemmProblem> g;
+    for (int q = 0; q < nsl; ++q) {
+      mss[q] = ms / kfull * (k1s[q] - k0s[q]);
+      S[q] = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * mss[q] * kd));
+      g.push_back(mk_gemm(sl[q].out, OP_N, nz, fd.p, OP_T, nz, S[q], kd, mss[q], kd, nz));   // S_s = Z_s L^T
+      g.back().exp_out = d_e;
+      flops_sub[b] += gemm_flops(g.back());
+    }
+    gemm_batch(ctx, g, st);
+    comm->allreduce_max(d_e, 1, ctx->stream);   // one range exponent for all of S
+    {
+      std::vector<Pow2Problem> p2;
+      for (int q = 0; q < nsl; ++q) p2.push_back(Pow2Problem{S[q], mss[q] * kd, d_e});
+      launch_pow2_apply(p2.data(), (int)p2.size(), *ctx->stager, ctx->stream);
+    }
+    cplx* W = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * kd * kd));
+    cplx* Li = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * kd * kd));
+    auto gram_sum = [&](const std::vector<cplx*>& X) {   // W = sum over all ranks' slices of X^H X
+      TTN_CUDA(cudaMemsetAsync(W, 0, sizeof(cplx) * kd * kd, ctx->stream));
+      for (int q = 0; q < nsl; ++q) {
+        std::vector<GemmProblem> gg{mk_gemm(X[q], OP_C, kd, X[q], OP_N, kd, W, kd, kd, kd, mss[q])};
+        gg[0].beta = make_double2(1.0, 0.0);
+        flops_sub[b] += gemm_flops(gg[0]);
+        gemm_batch(ctx, gg, st);
+      }
+      comm->allreduce_sum(reinterpret_cast<double*>(W), 2 * (size_t)kd * kd, ctx->stream);
+    };
+    auto solve = [&](const std::vector<cplx*>& X, std::vector<cplx*>& Y, int* info, double tol_rel) {
+      gram_sum(X);
+      PotriProblem pp{W, kd, (int)kd, 0, info, tol_rel, 0.0, Li};
+      launch_potri(&pp, 1, *ctx->stager, ctx->stream);
+      flops_inst[b].add_nongemm(8.0 * 2.0 * (kd * kd * kd / 3.0));
+      std::vector<GemmProblem> gg;
+      for (int q = 0; q < nsl; ++q) {
+        Y[q] = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * mss[q] * kd));
+        gg.push_back(mk_gemm(X[q], OP_N, kd, Li, OP_C, kd, Y[q], kd, mss[q], kd, kd));   // X L^-H
+        flops_sub[b] += gemm_flops(gg.back());
+      }
+      gemm_batch(ctx, gg, st);
+    };
+    solve(S, Q1, d_info, kCholTol);
+    solve(Q1, Q, d_info + 1, kCholTol * 1e-2);
+    ctx->ensure_small(sizeof(int) * 2);
+    int* hi = reinterpret_cast<int*>(ctx->hbuf);
+    TTN_CUDA(cudaMemcpyAsync(hi, d_info, sizeof(int) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (hi[0] != 0 || hi[1] != 0)
+      throw Error(TTN_ERR_NUMERIC, "rank-deficient S in a row-split final sweep (CholeskyQR2 pivot)");
+    if (r != kd) throw Error(TTN_ERR_UNSUPPORTED, "row-split final sweep expects r = kd");
+    // T'_i: scatter my slices' rows of Q into the zeroed tensor [d, r, rc...], then all-reduce
+    cplx* T = outs[b]->node(i);
+    int64_t te = d * r;
+    for (auto x : rc) te *= x;
+    TTN_CUDA(cudaMemsetAsync(T, 0, sizeof(cplx) * te, ctx->stream));
+    std::vector<PermProblem> pq;
+    std::vector<long long> dst(2 + rc.size());   // strides of T' [d, r, rc...]
+    {
+      long long s = 1;
+      for (int l = (int)rc.size() - 1; l >= 0; --l) {
+        dst[2 + l] = s;
+        s *= rc[l];
+      }
+      dst[1] = s;
+      dst[0] = s * r;
+    }
+    for (int q = 0; q < nsl; ++q) {
+      std::vector<int64_t> rcs = rc;
+      rcs[cpos] = k1s[q] - k0s[q];
+      PermProblem pp{};
+      pp.src = Q[q];
+      pp.dst = T + k0s[q] * dst[2 + cpos];
+      pp.rank = 2 + (int)rc.size();
+      if (pp.rank > 8) throw Error(TTN_ERR_UNSUPPORTED, "row split: too many legs");
+      pp.dims[0] = d;
+      pp.dims[1] = r;
+      long long srow = r;   // Q_s rows (d, rcs...), columns r
+      for (int l = (int)rcs.size() - 1; l >= 0; --l) {
+        pp.dims[2 + l] = rcs[l];
+        pp.sstride[2 + l] = srow;
+        srow *= rcs[l];
+      }
+      pp.sstride[0] = srow;
+      pp.sstride[1] = 1;
+      pp.dst_strided = 1;
+      pp.total = 1;
+      for (int x = 0; x < pp.rank; ++x) {
+        pp.dstride[x] = dst[x];
+        pp.total *= pp.dims[x];
+      }
+      pq.push_back(pp);
+    }
+    if (!pq.empty()) launch_permute(pq.data(), (int)pq.size(), *ctx->stager, ctx->stream);
+    comm->allreduce_sum(reinterpret_cast<double*>(T), 2 * (size_t)te, ctx->stream);
+    // R_i = sum_s Q_s^H Z_s
+    Fac& Ri = R[(size_t)b * n + i];
+    Ri.p = static_cast<cplx*>(ctx->env.alloc(sizeof(cplx) * r * nz));
+    Ri.k = r;
+    Ri.a = fd.a;
+    Ri.b = fd.b;
+    TTN_CUDA(cudaMemsetAsync(Ri.p, 0, sizeof(cplx) * r * nz, ctx->stream));
+    for (int q = 0; q < nsl; ++q) {
+      std::vector<GemmProblem> gg{mk_gemm(Q[q], OP_C, r, sl[q].out, OP_N, nz, Ri.p, nz, r, nz, mss[q])};
+      gg[0].beta = make_double2(1.0, 0.0);
+      flops_sub[b] += gemm_flops(gg[0]);
+      gemm_batch(ctx, gg, st);
+    }
+    comm->allreduce_sum(reinterpret_cast<double*>(Ri.p), 2 * (size_t)r * nz, ctx->stream);
+    ++split_inst[b];
+  };
+
   // ---------------- 3. final sweep (Eqs. 12-14) and 4. assembly, over the nodes selected
   auto final_sweep = [&](auto sel, bool sub) {
     HostScope hs_("final_sweep");
@@ -850,10 +1020,23 @@ void apply_core(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* co
           std::map<int, const Fac*> f;
           for (size_t l = 0; l < ch[i].size(); ++l) f[1 + (int)l] = &R[(size_t)b * n + ch[i][l]];
           cplx* out = (i == root) ? outs[b]->node(i) : nullptr;   // assembly: T'_root = Z_root
-          tasks.push_back(node_task(sts[b], ops[b], i, f, 0, out));
+          Task t = node_task(sts[b], ops[b], i, f, 0, out);
+          if (!sub && part.on && nslices >= 2 && i != root && !ch[i].empty()) {
+            int64_t ms = ref->phys[i], kw = 0;
+            for (size_t o = 2; o < t.ops.size(); ++o) {
+              ms *= t.ops[o].dims[0];
+              kw = std::max<int64_t>(kw, t.ops[o].dims[0]);
+            }
+            const Fac& fd = down[(size_t)b * n + i];
+            if (ms > fd.k && kw >= nslices && ms * fd.a * fd.b >= split_min && rb[b][i] == fd.k) {
+              final_split(b, i, t);   // heavy replicated node: rows split over the ranks
+              continue;
+            }
+          }
+          tasks.push_back(t);
           who.push_back({b, i});
         }
-      if (tasks.empty()) continue;
+      if (tasks.empty()) { ctx->scratch.reset(); continue; }
       ExecStats cs;
       contract_batch(ctx, tasks, cs);
       st.peak_entries = std::max(st.peak_entries, cs.peak_entries);

@@ -12,6 +12,7 @@
 #include "prof.h"
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 namespace tcbc {
 
@@ -474,6 +475,102 @@ __global__ void __launch_bounds__(256) geqr_q_grouped(const GeqrProblem* __restr
   }
 }
 
+
+// potrf_small followed by trtri_small in the same CTA (orders <= 64): the factor stays in
+// shared memory between the two, one launch instead of two (latency-bound QR / certificate
+// levels of the small-tree configs)
+__global__ void __launch_bounds__(256) potri_small(const PotriProblem* __restrict__ probs) {
+  const PotriProblem P = probs[blockIdx.x];
+  const int n = P.n, ldS = n + 1;
+  const long long ld = P.lda;
+  cplx* A = P.A;
+  extern __shared__ __align__(16) unsigned char ch_smem[];
+  cplx* S = reinterpret_cast<cplx*>(ch_smem);   // [n][n + 1], lower triangle: L
+  cplx* X = S + (size_t)n * ldS;                // [n][n + 1]: L^{-1}
+  cplx* R = X + (size_t)n * ldS;                // [n]: 1 / L[a][a]
+  __shared__ double red[32];
+  __shared__ int s_fail;
+  const int tid = threadIdx.x;
+  double md = -1e300;
+  for (int e = tid; e < n * n; e += 256) {
+    const int r = e / n, c = e % n;
+    if (c <= r) {
+      const cplx v = A[r * ld + c];
+      S[r * ldS + c] = v;
+      if (c == r) md = fmax(md, v.x);
+    }
+  }
+  md = block_max(md, red);
+  if (P.shift_rel > 0.0 && md > 0.0) {
+    const double sh = P.shift_rel * md;
+    for (int i = tid; i < n; i += 256) S[i * ldS + i].x += sh;
+    md += sh;
+  }
+  const double thresh = P.rel_tol * md;
+  if (tid == 0) s_fail = (md > 0.0 && isfinite(md)) ? 0 : 1;
+  __syncthreads();
+  for (int c = 0; c < n && !s_fail; ++c) {
+    const double d = S[c * ldS + c].x;
+    if (!(d > thresh) || !isfinite(d)) {
+      if (tid == 0) s_fail = c + 1;
+      break;
+    }
+    const double sd = sqrt(d), inv = 1.0 / sd;
+    for (int r = c + 1 + tid; r < n; r += 256) {
+      const cplx v = S[r * ldS + c];
+      S[r * ldS + c] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncthreads();
+    if (tid == 0) S[c * ldS + c] = make_double2(sd, 0.0);
+    for (int r = c + 1 + (tid >> 4); r < n; r += 16) {
+      const cplx lr = S[r * ldS + c];
+      for (int l = c + 1 + (tid & 15); l <= r; l += 16) {
+        const cplx u = cmulc(lr, S[l * ldS + c]);
+        S[r * ldS + l].x -= u.x;
+        S[r * ldS + l].y -= u.y;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0 && P.info) *P.info = s_fail;
+  if (s_fail) return;   // uniform
+  if (P.write_l)
+    for (int e = tid; e < n * n; e += 256) {
+      const int r = e / n, c = e % n;
+      A[r * ld + c] = c <= r ? S[r * ldS + c] : make_double2(0.0, 0.0);
+    }
+  for (int a = tid; a < n; a += 256) R[a] = cdiv(make_double2(1.0, 0.0), S[a * ldS + a]);
+  __syncthreads();
+  const int b = tid >> 2, sub = tid & 3, b0 = (tid >> 5) * 8;
+  if (b0 < n) {
+    if (sub == 0 && b < n)
+      for (int a = 0; a < b; ++a) X[a * ldS + b] = make_double2(0.0, 0.0);
+    __syncwarp();
+    for (int a = b0; a < n; ++a) {
+      const bool act = b < n && a >= b;
+      double sr = 0.0, si = 0.0;
+      if (act)
+        for (int j = b + sub; j < a; j += 4) {
+          const cplx u = cmul(S[a * ldS + j], X[j * ldS + b]);
+          sr += u.x;
+          si += u.y;
+        }
+      sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+      si += __shfl_xor_sync(0xffffffffu, si, 1);
+      sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+      si += __shfl_xor_sync(0xffffffffu, si, 2);
+      if (act && sub == 0) X[a * ldS + b] = cmul(make_double2((a == b ? 1.0 : 0.0) - sr, -si), R[a]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += 256) {
+    const int r = e / n, c = e % n;
+    P.Linv[r * ld + c] = X[r * ldS + c];
+  }
+}
+
 // one CTA per Gram: ||Li||_F^2 over the lower triangle and tr W, then the certificate
 __global__ void __launch_bounds__(256) chol_certify(const CertProblem* __restrict__ probs) {
   const CertProblem P = probs[blockIdx.x];
@@ -546,6 +643,32 @@ void launch_exact_factor(ExactFactorProblem* h, int n, Stager& st, cudaStream_t 
   prof_begin(s);
   exact_factor<<<dim3((unsigned)std::min<long long>((mx + 255) / 256, 64), n), 256, 0, s>>>(d);
   prof_end(s, "misc", 0.0, 32.0 * (double)mx * n);
+  count_launch();
+}
+
+void launch_potri(PotriProblem* h, int n, Stager& st, cudaStream_t s) {
+  if (n == 0) return;
+  int mx = 1;
+  for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].n);
+  if (mx > CH_SMALL) {   // blocked kernels, two launches
+    std::vector<PotrfProblem> pf(n);
+    std::vector<TrtriProblem> tr(n);
+    for (int i = 0; i < n; ++i) {
+      pf[i] = PotrfProblem{h[i].A, h[i].lda, h[i].n, 0, h[i].info, h[i].rel_tol, h[i].shift_rel};
+      tr[i] = TrtriProblem{h[i].A, h[i].Linv, h[i].lda, h[i].n, 0};
+    }
+    launch_potrf(pf.data(), n, st, s);
+    launch_trtri(tr.data(), n, st, s);
+    return;
+  }
+  const PotriProblem* d = static_cast<const PotriProblem*>(st.put(h, sizeof(PotriProblem) * n));
+  double fl = 0.0;
+  for (int i = 0; i < n; ++i) fl += 8.0 * 2.0 * (double)h[i].n * h[i].n * h[i].n / 6.0;
+  const size_t sm = (2 * (size_t)mx * (mx + 1) + mx) * sizeof(cplx);
+  func_smem(potri_small, (2 * (size_t)CH_SMALL * (CH_SMALL + 1) + CH_SMALL) * sizeof(cplx));
+  prof_begin(s);
+  potri_small<<<n, 256, sm, s>>>(d);
+  prof_end(s, "potrf", fl, 0.0);
   count_launch();
 }
 

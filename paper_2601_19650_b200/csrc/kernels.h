@@ -61,6 +61,9 @@ struct PermProblem {
   int conj;
   long long dims[8];
   long long sstride[8];
+  int dst_strided;     // 0: dst contiguous; 1: dst offset = sum_r index_r * dstride[r] (a scatter)
+  int pad_;
+  long long dstride[8];
 };
 
 // Top-kmax eigenpairs of an n x n Hermitian matrix A (full storage, row-major, lda = n;
@@ -91,6 +94,7 @@ struct HeevProblem {
 size_t heev_work_doubles(int n, int kmax);
 size_t heev_smem_bytes(int n, int kmax);
 int heev_max_n();
+int heev_small_n();   // Grams up to this order take the one-launch Jacobi kernel
 
 // In-place lower Cholesky A + s I = L L^H of an n x n Hermitian matrix (full storage, ld = lda;
 // s = shift_rel * max diag, 0 by default: the shifted first pass of CholeskyQR3);
@@ -103,6 +107,20 @@ struct PotrfProblem {
   int* info;
   double rel_tol;
   double shift_rel;
+};
+
+// potrf then trtri of the same matrix (Linv = L^{-1} of A + s I = L L^H); one fused launch for
+// orders <= 64 (the factor stays in shared memory), the blocked pair otherwise.  A receives L
+// when write_l (always for the blocked pair).  Linv is unspecified when info != 0.
+struct PotriProblem {
+  cplx* A;
+  long long lda;
+  int n;
+  int write_l;
+  int* info;
+  double rel_tol;
+  double shift_rel;
+  cplx* Linv;
 };
 
 // Linv = L^{-1} (n x n lower, full storage, upper zeroed).
@@ -178,6 +196,8 @@ void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s,
                  const std::function<void()>& values_ready = std::function<void()>());
 void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s);
+struct PotriProblem;
+void launch_potri(PotriProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_chol_certify(CertProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_exact_factor(ExactFactorProblem* h, int n, Stager& st, cudaStream_t s);
 void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s);

@@ -49,16 +49,17 @@ __global__ void permute_grouped(const PermProblem* __restrict__ probs, int nprob
        g += (long long)gridDim.x * blockDim.x) {
     int pi = find_by_start(probs, nprob, g);
     const PermProblem& P = probs[pi];
-    long long i = g - P.start, rem = i, off = 0;
+    long long i = g - P.start, rem = i, off = 0, doff = 0;
     for (int r = P.rank - 1; r >= 0; --r) {
       long long d = P.dims[r];
       long long x = rem % d;
       rem /= d;
       off += x * P.sstride[r];
+      doff += x * P.dstride[r];
     }
     cplx v = P.src[off];
     if (P.conj) v.y = -v.y;
-    P.dst[i] = v;
+    P.dst[P.dst_strided ? doff : i] = v;
   }
 }
 

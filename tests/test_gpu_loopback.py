@@ -106,3 +106,24 @@ def test_loopback_config4_two_ranks(P, parts):
         assert abs(norm(a) ** 2 - gold["phi_norm2"]) <= 1e-10 * gold["phi_norm2"]
         assert distances(a, b)[0] <= 1e-12
         assert (rep["split_compresses"] > 0) == (parts == 4)
+
+
+@pytest.mark.parametrize("world,slices", [(2, 4), (3, 3)])
+def test_loopback_row_splits_match_plain_apply(P, world, slices, monkeypatch):
+    """TTN_PARTITION_SLICES forces the row splits on small trees: the replicated top's Grams
+    (split_rows) and its final sweep (final_split: CholeskyQR2 and R from all-reduced partial
+    sums, the new tensors scattered and all-reduced) over `world` ranks, several slices each."""
+    from oracle import TTN
+    from ._helpers import distances
+    monkeypatch.setenv("TTN_PARTITION_SLICES", str(slices))
+    parent = W.complete_binary(63)
+    inst = W.configs.random_instance(parent, [2] * 63, 3, 2, 4, seed=8)
+    ref, rep0 = _plain(P, inst, 4)
+    outs = _ranks(P, inst, world, 4, 4)
+    b = TTN(parent, ref, "state")
+    for tens, rep in outs:
+        a = TTN(parent, tens, "state")
+        assert a.bonds() == b.bonds()
+        assert distances(a, b)[0] <= 1e-14
+        assert rep["split_compresses"] > 0
+        assert abs(rep["norm"] - rep0["norm"]) <= 1e-12 * rep0["norm"]

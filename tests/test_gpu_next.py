@@ -134,3 +134,39 @@ def test_f2_paper_random_structures_vs_oracle(P, ctx, kind, mb):
     assert abs(norm(phi_g) ** 2 - norm(phi_o) ** 2) <= 1e-10 * norm(phi_o) ** 2
     s = P.ttn_sandwich(ctx, out, op_g, st_g)                 # P2 on the GPU
     assert abs(s - rep["norm"] ** 2) <= 1e-11 * rep["norm"] ** 2
+
+
+@pytest.mark.parametrize("kind", ["mps", "t3ns_chains", "t3ns_leaves"])
+def test_f1_paper_circuit_matches_oracle_and_returns(P, ctx, kind):
+    """f1 (§IV.B, reading A25): 27 qubits, N = 3 tree-like batches of
+    CNOT (V1 x V2) gates, U then U^dagger, one TTNO per circuit level.  At D-bar = 10 (truncated)
+    the GPU state after every level matches the oracle's (1 - cos <= 1e-10, same bonds) and
+    both give the same Err; at D-bar = 200 the T3NS layouts return |0...0> to rounding (the
+    paper's "converge to numerical error", P:357)."""
+    import workloads.circuit_f1 as F
+    from ._helpers import stable_distances
+    st = F.structure_for(kind, 27)
+    levels = F.full_circuit_levels(27, 3, seed=0)
+    zero = TTN(st.parent, F.zero_state(st))
+    for dbar in (10, 200):
+        if dbar == 200 and kind == "mps":
+            continue
+        cur = P.ttn_create(ctx, P.TTN_STATE, st.parent, st.phys, [1] * st.n, F.zero_state(st))
+        ref = zero.copy()
+        for li, lev in enumerate(levels):
+            o, b = F.level_operator(st, lev)
+            oh = P.ttn_create(ctx, P.TTN_OPERATOR, st.parent, st.phys, b, o)
+            cur, rep = P.cbc_apply(ctx, oh, cur, dbar)
+            if dbar == 10:
+                ref = oracle_cbc(TTN(st.parent, o, "operator"), ref, dbar)
+                if li % 6 == 5 or li == len(levels) - 1:
+                    g = to_oracle(P, cur, st.parent)
+                    assert g.bonds() == ref.bonds(), (li, g.bonds(), ref.bonds())
+                    assert stable_distances(g, ref)[0] <= 1e-10, li
+        g = to_oracle(P, cur, st.parent)
+        err = stable_distances(g, zero)[1]
+        if dbar == 10:
+            assert abs(err - stable_distances(ref, zero)[1]) <= 1e-8
+            assert err > 1e-6                     # D-bar = 10 truncates
+        else:
+            assert err <= 1e-10, err
