@@ -504,7 +504,7 @@ __device__ void tridiag_stats(const HeevProblem& P, double trace) {
 }
 
 
-// ---------------------------------------------------------------- K0: small Grams (n <= 32)
+// ---------------------------------------------------------------- K0: tiny Grams (n <= 12)
 // "n <= 64: batched cyclic Jacobi per CTA in shared memory".  One warp per
 // Gram (lane = row), the Hermitian matrix and the eigenvector matrix in shared memory (odd
 // row stride: conflict-free column access), parallel cyclic Jacobi with the round-robin
@@ -513,7 +513,10 @@ __device__ void tridiag_stats(const HeevProblem& P, double trace) {
 // Then the descending sort, the truncation decision of heev_finish (k, discarded weight,
 // dropped rows zeroed), the pow2 unscale and the exact-factor skip -- the whole K1..K7
 // pipeline of a small Gram in ONE launch (latency-bound trees: configs 1, 5).
-constexpr int JAC_MAX_N = 32;
+constexpr int JAC_MAX_N = 32;    // the kernel's limit
+// routing limit (measured): Jacobi costs ~64 n^3 flops per Gram against the pipeline's
+// ~(4/3) n^3, so it wins only where the pipeline's nine launches dominate -- tiny Grams
+constexpr int JAC_ROUTE_N = 12;
 constexpr int JAC_WARPS = 4;
 __host__ __device__ inline int jac_ld(int n) { return n | 1; }
 // per warp: A and V (n x LD complex), then per pair c, s, Re / Im e^{-i phi} (4 doubles) and
@@ -1702,7 +1705,7 @@ size_t heev_smem_bytes(int n, int kmax) {
 }
 
 int heev_max_n() { return HEEV_MAX_N; }
-int heev_small_n() { return JAC_MAX_N; }
+int heev_small_n() { return JAC_ROUTE_N; }
 
 namespace {
 template <int CS>
@@ -1739,7 +1742,7 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
   if (nin == 0) return;
   // K0: Grams of order <= 32 in one launch (warp per Gram); the rest take K1..K7
   std::vector<HeevProblem> small, rest;
-  for (int i = 0; i < nin; ++i) (hin[i].n <= JAC_MAX_N ? small : rest).push_back(hin[i]);
+  for (int i = 0; i < nin; ++i) (hin[i].n <= JAC_ROUTE_N ? small : rest).push_back(hin[i]);
   if (!small.empty()) {
     int nmax = 1;
     for (auto& p : small) nmax = std::max(nmax, p.n);
