@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(JAC_WARPS * 32) heev_jacobi(const HeevProblem*
   }
   fro = warp_sum(fro);
   tr = warp_sum(tr);
+  const double afro = sqrt(fro);
   __syncwarp();
   const int m = n + (n & 1), t = m - 1, np = m / 2;
   for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
@@ -573,9 +574,10 @@ __global__ void __launch_bounds__(JAC_WARPS * 32) heev_jacobi(const HeevProblem*
       }
     }
     off = warp_sum(off);
-    // off-diagonal mass at the rounding level of the rotations (a few ulps of ||A||_F): the
-    // eigenvector error is then ~1e-15 ||A|| / gap, far inside the parity budget
-    if (!(off > 1e-30 * fro)) break;
+    // off-diagonal mass at the rounding level of the rotations (1e-14 ||A||_F): the eigenvector
+    // error is then ~1e-14 ||A|| / gap, far inside the parity budget; rotations below it only
+    // reshuffle rounding noise between (near-)zero eigenvalues and never converge further
+    if (!(off > 1e-28 * fro)) break;
     for (int r = 0; r < t; ++r) {
       if (lane < np) {
         int p, q;
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(JAC_WARPS * 32) heev_jacobi(const HeevProblem*
           const double ar = hypot(apq.x, apq.y);
           const double dp = A[p * LD + p].x, dq = A[q * LD + q].x;
           // negligible: below the rounding of the diagonal pair (classical Jacobi skip test)
-          if (ar > 1e-17 * sqrt(fabs(dp * dq)) && ar > 1e-300) {
+          if (ar > 1e-17 * sqrt(fabs(dp * dq)) && ar > 1e-16 * afro && ar > 1e-300) {
             const double zeta = (dq - dp) / (2.0 * ar);
             const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             c = 1.0 / sqrt(1.0 + tt * tt);
