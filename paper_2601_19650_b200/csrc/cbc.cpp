@@ -209,8 +209,9 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
       flops_inst[J.inst] += 8.0 * (double)kmax * n * m;
     }
     st.peak_entries = std::max(st.peak_entries, nn * nn);
-    // (Grams of order <= heev_small_n() take the one-launch Jacobi solver: nothing to save)
-    if (mine(j) && tol == 0.0 && kmax == nn && nn > heev_small_n() && !chfsi_applicable((int)nn, (int)kmax) && (m >= n || J.X)) {
+    // (below order 32 the eigensolver is launch-latency bound: the shortcut's extra launches
+    // would cost more than the stages it skips)
+    if (mine(j) && tol == 0.0 && kmax == nn && nn > std::max(32, heev_small_n()) && !chfsi_applicable((int)nn, (int)kmax) && (m >= n || J.X)) {
       cplx* Wc = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
       cplx* Li = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nn));
       PermProblem pp{};

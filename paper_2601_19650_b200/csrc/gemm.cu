@@ -25,7 +25,10 @@
 #include "prof.h"
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <stdexcept>
+#include <string>
 #include <vector>
 
 namespace tcbc {
@@ -545,6 +548,42 @@ void gemm_from_ops(GemmProblem& g, int opA, long long lda, int opB, long long ld
   g.conjB = (opB & 2) ? 1 : 0;
 }
 
+
+// ---------------------------------------------------------------- forked variant streams
+constexpr int kAux = 3;
+struct AuxStreams {
+  int device = -1;
+  cudaStream_t s[kAux] = {};
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[kAux] = {};
+};
+#define TTN_GEMM_CHECK(x)                                                                   \
+  do {                                                                                      \
+    cudaError_t e__ = (x);                                                                  \
+    if (e__ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+// per host thread and device (worker contexts run on their own threads)
+AuxStreams& aux_streams() {
+  thread_local std::vector<AuxStreams> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (auto& a : per_dev)
+    if (a.device == dev) return a;
+  per_dev.emplace_back();
+  AuxStreams& a = per_dev.back();
+  a.device = dev;
+  for (int i = 0; i < kAux; ++i) {
+    TTN_GEMM_CHECK(cudaStreamCreateWithFlags(&a.s[i], cudaStreamNonBlocking));
+    TTN_GEMM_CHECK(cudaEventCreateWithFlags(&a.join[i], cudaEventDisableTiming));
+  }
+  TTN_GEMM_CHECK(cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming));
+  return a;
+}
+bool getenv_fork() {
+  static const bool off = getenv("TTN_GEMM_NO_FORK") != nullptr;
+  return !off;
+}
+
 void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws) {
   HostScope hs_("launch_gemm");
   // group by tile shape (least padded work) and shared-memory layouts; Hermitian products take
@@ -637,11 +676,31 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
     }
   }
   const GemmProblem* d = static_cast<const GemmProblem*>(st.commit(ord, stage_bytes));
-#define TCBC_LV(G, BM, BN, WM, WN)                                                             \
-  launch_variant<BM, BN, WM, WN, false, false>(d + off[G + 0], cnt[G + 0], tiles[G + 0], s); \
-  launch_variant<BM, BN, WM, WN, false, true>(d + off[G + 1], cnt[G + 1], tiles[G + 1], s);  \
-  launch_variant<BM, BN, WM, WN, true, false>(d + off[G + 2], cnt[G + 2], tiles[G + 2], s);  \
-  launch_variant<BM, BN, WM, WN, true, true>(d + off[G + 3], cnt[G + 3], tiles[G + 3], s);
+  // Variant kernels of one launch set are independent (distinct outputs); when several are
+  // non-empty they run on forked streams so one persistent kernel's tail overlaps the next
+  // kernel instead of idling SMs (fork / join by events: also valid inside a graph capture).
+  int nv = 0;
+  for (int g = 0; g < NV; ++g) nv += (cnt[g] > 0 && tiles[g] > 0) ? 1 : 0;
+  AuxStreams& aux = aux_streams();
+  const bool fork = nv > 1 && getenv_fork();
+  if (fork) TTN_GEMM_CHECK(cudaEventRecord(aux.fork, s));
+  int used = 0;
+  auto pick = [&](int g) -> cudaStream_t {
+    if (!fork || cnt[g] == 0 || tiles[g] == 0) return s;
+    if (used == 0) {   // the first non-empty variant stays on s
+      ++used;
+      return s;
+    }
+    cudaStream_t a = aux.s[(used - 1) % kAux];
+    if (used <= kAux) TTN_GEMM_CHECK(cudaStreamWaitEvent(a, aux.fork, 0));
+    ++used;
+    return a;
+  };
+#define TCBC_LV(G, BM, BN, WM, WN)                                                                      \
+  launch_variant<BM, BN, WM, WN, false, false>(d + off[G + 0], cnt[G + 0], tiles[G + 0], pick(G + 0)); \
+  launch_variant<BM, BN, WM, WN, false, true>(d + off[G + 1], cnt[G + 1], tiles[G + 1], pick(G + 1));  \
+  launch_variant<BM, BN, WM, WN, true, false>(d + off[G + 2], cnt[G + 2], tiles[G + 2], pick(G + 2));  \
+  launch_variant<BM, BN, WM, WN, true, true>(d + off[G + 3], cnt[G + 3], tiles[G + 3], pick(G + 3));
   prof_begin(s);
   TCBC_LV(0, 64, 64, 2, 2)
   TCBC_LV(4, 128, 32, 4, 1)
@@ -649,6 +708,11 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
   TCBC_LV(12, 128, 16, 4, 1)
   TCBC_LV(16, 16, 128, 1, 4)
 #undef TCBC_LV
+  if (fork)   // join: s waits for every aux stream used
+    for (int a = 0; a < std::min(used - 1, kAux); ++a) {
+      TTN_GEMM_CHECK(cudaEventRecord(aux.join[a], aux.s[a]));
+      TTN_GEMM_CHECK(cudaStreamWaitEvent(s, aux.join[a], 0));
+    }
   prof_end(s, "zgemm", flops, bytes);
   if (nsplit > 0) {
     long long mx = 0;

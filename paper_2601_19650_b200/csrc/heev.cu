@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace tcbc {
@@ -514,9 +515,14 @@ __device__ void tridiag_stats(const HeevProblem& P, double trace) {
 // dropped rows zeroed), the pow2 unscale and the exact-factor skip -- the whole K1..K7
 // pipeline of a small Gram in ONE launch (latency-bound trees: configs 1, 5).
 constexpr int JAC_MAX_N = 32;    // the kernel's limit
-// routing limit (measured): Jacobi costs ~64 n^3 flops per Gram against the pipeline's
-// ~(4/3) n^3, so it wins only where the pipeline's nine launches dominate -- tiny Grams
-constexpr int JAC_ROUTE_N = 12;
+// routing limit: measured slower than the tridiagonal pipeline at every order (a warp-serial
+// round costs ~1 us, 5-8 sweeps of n - 1 rounds: ~85 us for n = 12 against the pipeline's
+// ~35 us; ~64 n^3 flops against ~(4/3) n^3), so it is off by default; TTN_JACOBI_MAX_N = m
+// routes Grams of order <= m (<= 32) to it for measurement
+inline int jac_route_n() {
+  static const int v = getenv("TTN_JACOBI_MAX_N") ? std::min(atoi(getenv("TTN_JACOBI_MAX_N")), JAC_MAX_N) : 0;
+  return v;
+}
 constexpr int JAC_WARPS = 4;
 __host__ __device__ inline int jac_ld(int n) { return n | 1; }
 // per warp: A and V (n x LD complex), then per pair c, s, Re / Im e^{-i phi} (4 doubles) and
@@ -1707,7 +1713,7 @@ size_t heev_smem_bytes(int n, int kmax) {
 }
 
 int heev_max_n() { return HEEV_MAX_N; }
-int heev_small_n() { return JAC_ROUTE_N; }
+int heev_small_n() { return jac_route_n(); }
 
 namespace {
 template <int CS>
@@ -1744,7 +1750,8 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
   if (nin == 0) return;
   // K0: Grams of order <= 32 in one launch (warp per Gram); the rest take K1..K7
   std::vector<HeevProblem> small, rest;
-  for (int i = 0; i < nin; ++i) (hin[i].n <= JAC_ROUTE_N ? small : rest).push_back(hin[i]);
+  const int jn = jac_route_n();
+  for (int i = 0; i < nin; ++i) (hin[i].n <= jn ? small : rest).push_back(hin[i]);
   if (!small.empty()) {
     int nmax = 1;
     for (auto& p : small) nmax = std::max(nmax, p.n);
