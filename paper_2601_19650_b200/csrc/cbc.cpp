@@ -53,6 +53,12 @@ struct CompressJob {
   cplx* G_pre = nullptr;   // row-split compress: the (already range-scaled) Gram X^H X; G route only
 };
 
+struct LevelScratch : Scratch {   // the ctx's per-level arena as launcher workspace
+  Arena& a;
+  explicit LevelScratch(Arena& ar) : a(ar) {}
+  void* get(size_t bytes) override { return a.alloc(bytes); }
+};
+
 struct QRJob {
   const cplx* S;     // m x kd
   int64_t m, kd;
@@ -256,7 +262,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
         if (chfsi_applicable(h.n, h.kmax)) large.push_back(&h);
         else small.push_back(h);
       }
-      if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream);
+      LevelScratch lws(ctx->scratch);
+      if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream, {}, &lws);
       if (!large.empty()) {
         *spec->host_synced = true;
         chfsi_heev(ctx, large, st);
@@ -304,7 +311,8 @@ void compress_batch(ttn_ctx_s* ctx, std::vector<CompressJob>& jobs, int64_t max_
         ctx->mark_ranks();
         early = true;
       };
-    if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream, ready);
+    LevelScratch lws(ctx->scratch);
+    if (!small.empty()) launch_heev(small.data(), (int)small.size(), *ctx->stager, ctx->stream, ready, &lws);
     else if (ready) ready();
     chfsi_heev(ctx, large, st);
   }

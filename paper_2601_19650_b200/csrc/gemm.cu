@@ -584,7 +584,7 @@ bool getenv_fork() {
   return !off;
 }
 
-void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws) {
+void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws, const char* family) {
   HostScope hs_("launch_gemm");
   // group by tile shape (least padded work) and shared-memory layouts; Hermitian products take
   // the square tile (lower-triangle tiles only); problems that cannot fill the GPU with output
@@ -713,7 +713,7 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws)
       TTN_GEMM_CHECK(cudaEventRecord(aux.join[a], aux.s[a]));
       TTN_GEMM_CHECK(cudaStreamWaitEvent(s, aux.join[a], 0));
     }
-  prof_end(s, "zgemm", flops, bytes);
+  prof_end(s, family, flops, bytes);
   if (nsplit > 0) {
     long long mx = 0;
     for (int i = total; i < total + nsplit; ++i) mx = std::max<long long>(mx, (long long)ord[i].M * ord[i].N);

@@ -1395,6 +1395,71 @@ __global__ void heev_backtr(const HeevProblem* __restrict__ probs, int nprob, in
   }
 }
 
+
+// ---------------------------------------------------------------- K5 (blocked): WY back-transform
+// V = Q Z with Q = H_0 ... H_{n-2} applied as blocks of WY_NB reflectors on the DMMA GEMM kernel
+// (SURVEY §8 a6 "DMMA back-transform"): Q_b = I - Y_b T_b Y_b^H (compact WY, zlarft forward
+// columnwise), Vt <- Vt - ((Vt conj(Y_b)) T_b^T) Y_b^T for b = last .. 0.  The reflectors are
+// the rows of A (v_j in row j, columns j+1.., v_j[j+1] = 1): wy_prep zeroes the rest of each
+// row so a block of rows IS Y_b^T, and starts Vt from the tridiagonal eigenvectors Z.
+constexpr int WY_NB = 64;
+constexpr int WY_MIN_N = 96;   // below: the register / shared-memory kernel (fewer launches)
+
+__global__ void wy_prep(const HeevProblem* __restrict__ probs) {
+  const HeevProblem P = probs[blockIdx.x];
+  if (P.skip && *P.skip) return;
+  const int n = P.n, kmax = P.kmax;
+  const int k = P.k_out ? *P.k_out : kmax;
+  const double* Z = P.work + 2 * n + 8;
+  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e - (long long)r * n);
+    if (c <= r || r == n - 1) P.A[e] = make_double2(0.0, 0.0);
+  }
+  for (long long e = threadIdx.x; e < (long long)kmax * n; e += blockDim.x) {
+    const int t = (int)(e / n), i = (int)(e - (long long)t * n);
+    P.Vt[e] = make_double2(t < k ? Z[(size_t)i * kmax + t] : 0.0, 0.0);
+  }
+}
+
+struct WyBlock {
+  const cplx* G;      // C[c'][c] = sum_i Y[i][c']^* ... (GEMM of the block's rows), nbb x nbb
+  cplx* T;            // nbb x nbb upper triangular, ld WY_NB
+  const cplx* tau;    // tau of the block's first reflector
+  const int* skip;
+  int nbb;
+  int pad_;
+};
+
+// one warp per block: T[c][c] = tau_c, T[r][c] = -tau_c sum_{r<=q<c} T[r][q] u_q,
+// u_q = (Y^H Y)[q][c] = conj(G[q][c])
+__global__ void wy_larft(const WyBlock* __restrict__ blks, int nb) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= nb) return;
+  const WyBlock B = blks[w];
+  if (B.skip && *B.skip) return;
+  const int m = B.nbb;
+  for (int c = 0; c < m; ++c) {
+    const cplx tc = B.tau[c];
+    for (int r = lane; r < m; r += 32) {
+      cplx v = make_double2(0.0, 0.0);
+      if (r < c) {
+        double sr = 0.0, si = 0.0;
+        for (int q = r; q < c; ++q) {
+          const cplx t = B.T[r * WY_NB + q];
+          const cplx g = B.G[q * m + c];          // u_q = conj(g)
+          sr += t.x * g.x + t.y * g.y;
+          si += t.y * g.x - t.x * g.y;
+        }
+        v = make_double2(-(tc.x * sr - tc.y * si), -(tc.x * si + tc.y * sr));
+      } else if (r == c) {
+        v = tc;
+      }
+      B.T[r * WY_NB + c] = v;
+    }
+    __syncwarp();
+  }
+}
+
 // K7: eigenvalues and discarded weight back to the unscaled data (HeevProblem::exp2)
 // what: 1 = the discarded weight (right after K6, so the host can read k and w early),
 // 2 = the eigenvalues (after inverse iteration, which shifts by the scaled values)
@@ -1745,7 +1810,85 @@ void launch_tridiag_cluster(const HeevProblem* d, int nprob, int cs, size_t smem
 }
 }  // namespace
 
-void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const std::function<void()>& values_ready) {
+
+namespace {
+// the WY back-transform of a launch (see wy_prep); Vt and A as in HeevProblem
+void backtr_wy(HeevProblem* h, int n, const HeevProblem* d, Stager& st, cudaStream_t s, Scratch* ws) {
+  prof_begin(s);
+  wy_prep<<<n, 256, 0, s>>>(d);
+  prof_end(s, "heev", 0.0, 0.0);
+  count_launch();
+  int maxb = 0;
+  std::vector<int> nblk(n);
+  for (int i = 0; i < n; ++i) {
+    nblk[i] = (h[i].n - 1 + WY_NB - 1) / WY_NB;
+    maxb = std::max(maxb, nblk[i]);
+  }
+  // Y_b^H Y_b of every block, then T_b
+  std::vector<GemmProblem> gg;
+  std::vector<WyBlock> wb;
+  std::vector<std::vector<cplx*>> T(n), G(n);
+  std::vector<cplx*> P1(n), P2(n);
+  for (int i = 0; i < n; ++i) {
+    const HeevProblem& p = h[i];
+    P1[i] = static_cast<cplx*>(ws->get(sizeof(cplx) * p.kmax * WY_NB));
+    P2[i] = static_cast<cplx*>(ws->get(sizeof(cplx) * p.kmax * WY_NB));
+    for (int b = 0; b < nblk[i]; ++b) {
+      const int j0 = b * WY_NB, nbb = std::min(WY_NB, p.n - 1 - j0);
+      cplx* Gb = static_cast<cplx*>(ws->get(sizeof(cplx) * nbb * nbb));
+      cplx* Tb = static_cast<cplx*>(ws->get(sizeof(cplx) * WY_NB * WY_NB));
+      const cplx* Yt = p.A + (size_t)j0 * p.n;
+      GemmProblem g{};
+      g.A = Yt; g.B = Yt; g.C = Gb; g.M = nbb; g.N = nbb; g.K = p.n;
+      gemm_from_ops(g, OP_N, p.n, OP_C, p.n, nbb);
+      g.alpha = make_double2(1.0, 0.0);
+      gg.push_back(g);
+      wb.push_back(WyBlock{Gb, Tb, p.tau + j0, p.skip, nbb, 0});
+      T[i].push_back(Tb);
+      G[i].push_back(Gb);
+    }
+  }
+  launch_gemm(gg.data(), (int)gg.size(), st, s, ws, "heev");
+  {
+    const WyBlock* dw = static_cast<const WyBlock*>(st.put(wb.data(), sizeof(WyBlock) * wb.size()));
+    prof_begin(s);
+    wy_larft<<<((int)wb.size() + 3) / 4, 128, 0, s>>>(dw, (int)wb.size());
+    prof_end(s, "heev", 0.0, 0.0);
+    count_launch();
+  }
+  for (int b = maxb - 1; b >= 0; --b) {
+    std::vector<GemmProblem> g1, g2, g3;
+    for (int i = 0; i < n; ++i) {
+      if (b >= nblk[i]) continue;
+      const HeevProblem& p = h[i];
+      const int j0 = b * WY_NB, nbb = std::min(WY_NB, p.n - 1 - j0);
+      const cplx* Yt = p.A + (size_t)j0 * p.n;
+      GemmProblem g{};
+      g.A = p.Vt; g.B = Yt; g.C = P1[i]; g.M = p.kmax; g.N = nbb; g.K = p.n;     // P1 = Vt conj(Y_b)
+      gemm_from_ops(g, OP_N, p.n, OP_C, p.n, nbb);
+      g.alpha = make_double2(1.0, 0.0);
+      g1.push_back(g);
+      GemmProblem g2p{};
+      g2p.A = P1[i]; g2p.B = T[i][b]; g2p.C = P2[i]; g2p.M = p.kmax; g2p.N = nbb; g2p.K = nbb;   // P2 = P1 T^T
+      gemm_from_ops(g2p, OP_N, nbb, OP_T, WY_NB, nbb);
+      g2p.alpha = make_double2(1.0, 0.0);
+      g2.push_back(g2p);
+      GemmProblem g3p{};
+      g3p.A = P2[i]; g3p.B = Yt; g3p.C = p.Vt; g3p.M = p.kmax; g3p.N = p.n; g3p.K = nbb;   // Vt -= P2 Y_b^T
+      gemm_from_ops(g3p, OP_N, nbb, OP_N, p.n, p.n);
+      g3p.alpha = make_double2(-1.0, 0.0);
+      g3p.beta = make_double2(1.0, 0.0);
+      g3.push_back(g3p);
+    }
+    launch_gemm(g1.data(), (int)g1.size(), st, s, ws, "heev");
+    launch_gemm(g2.data(), (int)g2.size(), st, s, ws, "heev");
+    launch_gemm(g3.data(), (int)g3.size(), st, s, ws, "heev");
+  }
+}
+}  // namespace
+
+void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const std::function<void()>& values_ready,
+                 Scratch* ws) {
   HostScope hs_("launch_heev");
   if (nin == 0) return;
   // K0: Grams of order <= 32 in one launch (warp per Gram); the rest take K1..K7
@@ -1868,6 +2011,18 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     } else {
       heev_orth<<<n, HEEV_THREADS, 0, s>>>(d);
     }
+  }
+  int mxn_all = 0;
+  for (int i = 0; i < n; ++i) mxn_all = std::max(mxn_all, h[i].n);
+  if (ws && mxn_all >= WY_MIN_N && !getenv("TTN_HEEV_NO_WY")) {
+    prof_end(s, "heev", fl, by);
+    count_launch(); count_launch(); count_launch(); count_launch(); count_launch();   // K2, K6, K7, K3, K4
+    backtr_wy(h, n, d, st, s, ws);
+    prof_begin(s);
+    heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n, 2);
+    prof_end(s, "heev", 0.0, 0.0);
+    count_launch();
+    return;
   }
   {
     int mxn = 0;

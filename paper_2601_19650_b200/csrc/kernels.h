@@ -188,13 +188,15 @@ struct Stager {
 };
 
 // Launchers fill the scheduling fields of the host problems, stage them, and launch.
-void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws = nullptr);
+// family: the ttn_profile family the launch set is timed under
+void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws = nullptr, const char* family = "zgemm");
 void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s);
 // values_ready (optional) is called once the ranks (k_out) and discarded weights (w_out) are
 // final in stream order -- before the eigenvector stages are enqueued -- so a caller can start
 // reading them while the vectors are still being computed.
+// ws (optional): workspace for the blocked (WY) back-transform on the GEMM kernel
 void launch_heev(HeevProblem* h, int n, Stager& st, cudaStream_t s,
-                 const std::function<void()>& values_ready = std::function<void()>());
+                 const std::function<void()>& values_ready = std::function<void()>(), Scratch* ws = nullptr);
 void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s);
 struct PotriProblem;
 void launch_potri(PotriProblem* h, int n, Stager& st, cudaStream_t s);
