@@ -2014,7 +2014,11 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
   }
   int mxn_all = 0;
   for (int i = 0; i < n; ++i) mxn_all = std::max(mxn_all, h[i].n);
-  if (ws && mxn_all >= WY_MIN_N && !getenv("TTN_HEEV_NO_WY")) {
+  // measured slower than heev_backtr_blk on every bench config (config 3: 962 -> 910 applies/s,
+  // config 5: 3428 -> 1219): the per-block GEMMs are tiny (k = 32 rows) and wy_larft is
+  // warp-serial; kept behind TTN_HEEV_WY=1 for measurement
+  static const bool wy_on = getenv("TTN_HEEV_WY") != nullptr;
+  if (ws && wy_on && mxn_all >= WY_MIN_N) {
     prof_end(s, "heev", fl, by);
     count_launch(); count_launch(); count_launch(); count_launch(); count_launch();   // K2, K6, K7, K3, K4
     backtr_wy(h, n, d, st, s, ws);
