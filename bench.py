@@ -375,8 +375,12 @@ def run_native(args, rank, world, local_rank):
         dist.barrier()
     launches = P.ttn_launch_count() - lc0
     clk = clocks.stop(local_rank) if clocks else None
-    # profiled pass: graphs off so the events bracket each launch set
+    # profiled pass: graphs off so the events bracket each launch set; one stream (concurrent
+    # worker sub-batches would stretch each kernel's event interval by sharing the GPU)
     prof_steps = args.steps if cfg in (3, 4) else min(args.steps, 5)
+    prof_workers = workers if cfg == 5 else 1
+    if prof_workers != workers:
+        P.ttn_ctx_set_workers(ctx, prof_workers)
     P.ttn_ctx_set_schedule(ctx, True, False)
     step()                                   # (re-plans without graphs; untimed)
     torch.cuda.synchronize()
@@ -392,6 +396,8 @@ def run_native(args, rank, world, local_rank):
     pe1.synchronize()
     prof_ms = pe0.elapsed_time(pe1)
     P.ttn_ctx_set_schedule(ctx, True, True)
+    if prof_workers != workers:
+        P.ttn_ctx_set_workers(ctx, workers)
     prof = {fam: P.ttn_profile_read(fam) for fam in ("all", "zgemm", "heev", "heev_large", "potrf", "trtri", "geqr", "permute",
                                                      "scale_rows", "misc", "gap_after_sync")}
     P.ttn_profile_enable(False)
@@ -546,7 +552,7 @@ def run_native(args, rank, world, local_rank):
                               "(4 n^2 K), factor / S / CholeskyQR / R products (ttn_cbc_report.flops_gemm_min); "
                               f"zgemm time = CUDA events around every launch set in a profiled pass of {prof_steps} "
                               "steps right after the timed region (speculative schedule without graphs)",
-                     "profiled_pass": {"steps": prof_steps, "ms_per_step": prof_ms / prof_steps,
+                     "profiled_pass": {"steps": prof_steps, "workers": prof_workers, "ms_per_step": prof_ms / prof_steps,
                                        "applies_per_s": p_applies / (prof_ms / 1000.0)},
                      "algorithmic_flops_per_step": gmin,
                      "kernel_efficiency": {"achieved": ach_exec, "frac": ach_exec / FP64_PEAK_TFLOPS,
