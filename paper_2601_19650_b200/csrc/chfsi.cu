@@ -58,6 +58,7 @@ struct LargeDev {
 };
 
 __global__ void random_fill(LargeDev* P) {
+  TCBC_PDL_WAIT();
   const LargeDev& L = P[blockIdx.y];
   const long long tot = (long long)L.n * L.p;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
@@ -67,6 +68,7 @@ __global__ void random_fill(LargeDev* P) {
 }
 
 __global__ void shift_copy(LargeDev* P) {
+  TCBC_PDL_WAIT();
   const LargeDev& L = P[blockIdx.y];
   const long long tot = (long long)L.n * L.n;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
@@ -77,6 +79,7 @@ __global__ void shift_copy(LargeDev* P) {
 }
 
 __global__ void col_scale(LargeDev* P) {
+  TCBC_PDL_WAIT();
   const LargeDev& L = P[blockIdx.y];
   const long long tot = (long long)L.n * L.p;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
@@ -96,6 +99,7 @@ struct ResDev {
 
 // one warp per (matrix, wanted Ritz pair): r_t = || W[:, t] - theta_t V[:, t] ||
 __global__ void ritz_residual(const ResDev* P, int nprob, int maxk) {
+  TCBC_PDL_WAIT();
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int b = gw / maxk, t = gw % maxk;
   if (b >= nprob) return;
@@ -122,6 +126,7 @@ struct FinDev {
 
 // trace, truncation decision and discarded weight (one thread per matrix), then Vt = V^T rows
 __global__ void large_finish(FinDev* P, int nprob) {
+  TCBC_PDL_WAIT();
   const int b = blockIdx.y;
   if (b >= nprob) return;
   const FinDev& F = P[b];
@@ -232,7 +237,7 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
     }
     LargeDev* d = static_cast<LargeDev*>(ctx->stager->put(L.data(), sizeof(LargeDev) * L.size()));
     (void)scale;
-    kern<<<dim3(296, (unsigned)L.size()), 256, 0, s>>>(d);
+    launch_k(kern, dim3(296, (unsigned)L.size()), 256, 0, s, d);
     count_launch();
   };
   // orthonormalise the unlocked tail V[:, c:p] of every active job in place: projected twice
@@ -306,7 +311,7 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
     gemm_batch(ctx, gv, st);
     const ResDev* d = static_cast<const ResDev*>(ctx->stager->put(rd.data(), sizeof(ResDev) * rd.size()));
     const long long warps = (long long)rd.size() * maxk;
-    ritz_residual<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(d, (int)rd.size(), maxk);
+    launch_k(ritz_residual, (unsigned)((warps * 32 + 255) / 256), 256, 0, s, d, (int)rd.size(), maxk);
     count_launch();
     for (Job* jp : act) {
       std::swap(jp->V, jp->V2);
@@ -468,7 +473,7 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
   std::vector<FinDev> F;
   for (auto& j : J) F.push_back(FinDev{j.hp->A, j.V, j.theta, *j.hp, j.p});
   FinDev* d = static_cast<FinDev*>(ctx->stager->put(F.data(), sizeof(FinDev) * F.size()));
-  large_finish<<<dim3(64, nb), 256, 0, s>>>(d, nb);
+  launch_k(large_finish, dim3(64, nb), 256, 0, s, d, nb);
   count_launch();
   static const bool dbg = getenv("TTN_DEBUG_CHFSI") != nullptr;
   if (dbg) fprintf(stderr, "[chfsi] %d matrices, n=%d p=%d kmax=%d: %d outer iterations\n", nb, J[0].n, J[0].p, J[0].kmax, iter);

@@ -59,6 +59,7 @@ constexpr int CH_THREADS = 512;
 // tensor cores (DMMA), reading the staged panel (one global read-modify-write per element per
 // panel instead of per column).  One CTA per matrix.
 __global__ void __launch_bounds__(CH_THREADS) potrf_grouped(const PotrfProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const PotrfProblem P = probs[blockIdx.x];
   const int n = P.n;
   const long long ld = P.lda;
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(CH_THREADS) potrf_grouped(const PotrfProblem* 
 constexpr int CH_SMALL = 64;
 
 __global__ void __launch_bounds__(256) potrf_small(const PotrfProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const PotrfProblem P = probs[blockIdx.x];
   const int n = P.n, ldS = n + 1;
   const long long ld = P.lda;
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(256) potrf_small(const PotrfProblem* __restric
 // substitution down the column, the column's inner products split over the four lanes and
 // combined by shuffles; diagonal reciprocals precomputed).
 __global__ void __launch_bounds__(4 * CH_SMALL) trtri_small(const TrtriProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const TrtriProblem P = probs[blockIdx.x];
   const int n = P.n, ldS = n + 1;
   const long long ld = P.ld;
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(4 * CH_SMALL) trtri_small(const TrtriProblem* 
 // every column c < R0 is formed as  Linv[R, c] = -D^{-1} sum_{j in [c, R0)} L[R, j] Linv[j, c]
 // (thread per column, Linv rows already written read back coalesced).
 __global__ void __launch_bounds__(CH_THREADS) trtri_grouped(const TrtriProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const TrtriProblem P = probs[blockIdx.x];
   const int n = P.n;
   const long long ld = P.ld;
@@ -372,6 +376,7 @@ __global__ void __launch_bounds__(CH_THREADS) trtri_grouped(const TrtriProblem* 
 // CholeskyQR2 flags a rank-deficient S (circuit layers, zero states): Householder gives an
 // isometry Q spanning range(S) for any rank, as the oracle's LAPACK QR does.
 __global__ void __launch_bounds__(256) geqr_q_grouped(const GeqrProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const GeqrProblem P = probs[blockIdx.x];
   const int m = P.m, k = P.k;
   cplx* A = P.A;
@@ -480,6 +485,7 @@ __global__ void __launch_bounds__(256) geqr_q_grouped(const GeqrProblem* __restr
 // shared memory between the two, one launch instead of two (latency-bound QR / certificate
 // levels of the small-tree configs)
 __global__ void __launch_bounds__(256) potri_small(const PotriProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const PotriProblem P = probs[blockIdx.x];
   const int n = P.n, ldS = n + 1;
   const long long ld = P.lda;
@@ -573,6 +579,7 @@ __global__ void __launch_bounds__(256) potri_small(const PotriProblem* __restric
 
 // one CTA per Gram: ||Li||_F^2 over the lower triangle and tr W, then the certificate
 __global__ void __launch_bounds__(256) chol_certify(const CertProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const CertProblem P = probs[blockIdx.x];
   __shared__ double red[32];
   const int n = P.n;
@@ -606,6 +613,7 @@ __global__ void __launch_bounds__(256) chol_certify(const CertProblem* __restric
 }
 
 __global__ void exact_factor(const ExactFactorProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const ExactFactorProblem P = probs[blockIdx.y];
   if (!*P.skip) return;
   const double sc = (P.mode == 0 && P.exp2) ? ldexp(1.0, pow2_effective(*P.exp2)) : 1.0;
@@ -630,7 +638,7 @@ void launch_chol_certify(CertProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   const CertProblem* d = static_cast<const CertProblem*>(st.put(h, sizeof(CertProblem) * n));
   prof_begin(s);
-  chol_certify<<<n, 256, 0, s>>>(d);
+  launch_k(chol_certify, n, 256, 0, s, d);
   prof_end(s, "potrf", 0.0, 0.0);
   count_launch();
 }
@@ -641,7 +649,7 @@ void launch_exact_factor(ExactFactorProblem* h, int n, Stager& st, cudaStream_t 
   for (int i = 0; i < n; ++i) mx = std::max<long long>(mx, (long long)h[i].rows * h[i].cols);
   const ExactFactorProblem* d = static_cast<const ExactFactorProblem*>(st.put(h, sizeof(ExactFactorProblem) * n));
   prof_begin(s);
-  exact_factor<<<dim3((unsigned)std::min<long long>((mx + 255) / 256, 64), n), 256, 0, s>>>(d);
+  launch_k(exact_factor, dim3((unsigned)std::min<long long>((mx + 255) / 256, 64), n), 256, 0, s, d);
   prof_end(s, "misc", 0.0, 32.0 * (double)mx * n);
   count_launch();
 }
@@ -667,7 +675,7 @@ void launch_potri(PotriProblem* h, int n, Stager& st, cudaStream_t s) {
   const size_t sm = (2 * (size_t)mx * (mx + 1) + mx) * sizeof(cplx);
   func_smem(potri_small, (2 * (size_t)CH_SMALL * (CH_SMALL + 1) + CH_SMALL) * sizeof(cplx));
   prof_begin(s);
-  potri_small<<<n, 256, sm, s>>>(d);
+  launch_k(potri_small, n, 256, sm, s, d);
   prof_end(s, "potrf", fl, 0.0);
   count_launch();
 }
@@ -678,7 +686,7 @@ void launch_geqr_q(GeqrProblem* h, int n, Stager& st, cudaStream_t s) {
   double fl = 0.0;
   for (int i = 0; i < n; ++i) fl += 16.0 * (double)h[i].m * h[i].k * h[i].k;
   prof_begin(s);
-  geqr_q_grouped<<<n, 256, 0, s>>>(d);
+  launch_k(geqr_q_grouped, n, 256, 0, s, d);
   prof_end(s, "geqr", fl, 0.0);
   count_launch();
 }
@@ -696,9 +704,9 @@ void launch_potrf(PotrfProblem* h, int n, Stager& st, cudaStream_t s) {
   if (mx <= CH_SMALL) {
     const size_t sm = (size_t)mx * (mx + 1) * sizeof(cplx);
     func_smem(potrf_small, (size_t)CH_SMALL * (CH_SMALL + 1) * sizeof(cplx));
-    potrf_small<<<n, 256, sm, s>>>(d);
+    launch_k(potrf_small, n, 256, sm, s, d);
   } else {
-    potrf_grouped<<<n, CH_THREADS, smem, s>>>(d);
+    launch_k(potrf_grouped, n, CH_THREADS, smem, s, d);
   }
   prof_end(s, "potrf", fl, 0.0);
   count_launch();
@@ -717,9 +725,9 @@ void launch_trtri(TrtriProblem* h, int n, Stager& st, cudaStream_t s) {
   if (mx <= CH_SMALL) {
     const size_t sm = (2 * (size_t)mx * (mx + 1) + mx) * sizeof(cplx);
     func_smem(trtri_small, (2 * (size_t)CH_SMALL * (CH_SMALL + 1) + CH_SMALL) * sizeof(cplx));
-    trtri_small<<<n, 4 * CH_SMALL, sm, s>>>(d);
+    launch_k(trtri_small, n, 4 * CH_SMALL, sm, s, d);
   } else {
-    trtri_grouped<<<n, CH_THREADS, smem, s>>>(d);
+    launch_k(trtri_grouped, n, CH_THREADS, smem, s, d);
   }
   prof_end(s, "trtri", fl, 0.0);
   count_launch();

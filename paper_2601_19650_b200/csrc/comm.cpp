@@ -152,6 +152,7 @@ namespace {
 
 template <typename T, int OP>   // OP 0: sum, 1: max
 __global__ void loop_reduce(T* __restrict__ out, const T* const* __restrict__ in, int world, size_t n) {
+  TCBC_PDL_WAIT();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     T v = in[0][i];
     for (int r = 1; r < world; ++r) v = OP == 0 ? v + in[r][i] : (in[r][i] > v ? in[r][i] : v);
@@ -209,7 +210,7 @@ struct LoopComm : Comm {
     std::vector<void*> hp(g->ptr.begin(), g->ptr.end());
     TTN_CUDA(cudaMemcpyAsync(dptrs, hp.data(), sizeof(void*) * world, cudaMemcpyHostToDevice, s));
     const int blocks = (int)std::min<size_t>((n + 255) / 256, 1184);
-    loop_reduce<T, OP><<<blocks, 256, 0, s>>>(static_cast<T*>(tmp), reinterpret_cast<const T* const*>(dptrs), world, n);
+    launch_k(loop_reduce<T, OP>, blocks, 256, 0, s, static_cast<T*>(tmp), reinterpret_cast<const T* const*>(dptrs), world, n);
     TTN_CUDA(cudaGetLastError());
     TTN_CUDA(cudaStreamSynchronize(s));   // hp (pageable) is read by the copy above
     done(s);

@@ -113,6 +113,7 @@ __device__ __forceinline__ int find_problem(const GemmProblem* p, int n, int til
 template <int BM, int BN, int WGM, int WGN, bool AKM, bool BNM, int ST, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) zgemm_grouped(const GemmProblem* __restrict__ probs, int nprob,
                                                             int total_tiles) {
+  TCBC_PDL_WAIT();
   using C_ = Cfg<BM, BN, AKM, BNM, ST>;
   constexpr int WTM = BM / WGM, WTN = BN / WGN;     // warp tile
   constexpr int TM = WTM / 8, TN = WTN / 8;         // DMMA tiles per warp
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(THREADS, MINB) zgemm_grouped(const GemmProblem
 
 // split-k reduction: C = alpha * sum_s W_s + beta * C (C through its strided legs)
 __global__ void zgemm_splitk_reduce(const GemmProblem* __restrict__ probs, int nprob) {
+  TCBC_PDL_WAIT();
   const GemmProblem& P = probs[blockIdx.y];
   const long long MN = (long long)P.M * P.N;
   const cplx al = P.alpha, be = P.beta;
@@ -516,7 +518,7 @@ void launch_variant(const GemmProblem* d, int n, int tiles, cudaStream_t s) {
   static_assert(MINB * C_::BYTES <= 227 * 1024, "shared memory for the resident CTAs");
   func_smem(zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB>, C_::BYTES);
   const int grid = std::min(tiles, MINB * 148);   // persistent: MINB resident CTAs per SM
-  zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB><<<grid, THREADS, C_::BYTES, s>>>(d, n, tiles);
+  launch_k(zgemm_grouped<BM, BN, WGM, WGN, AKM, BNM, ST, MINB>, grid, THREADS, C_::BYTES, s, d, n, tiles);
   count_launch();
 }
 
@@ -719,7 +721,7 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws,
     for (int i = total; i < total + nsplit; ++i) mx = std::max<long long>(mx, (long long)ord[i].M * ord[i].N);
     const int gx = (int)std::min<long long>((mx + 255) / 256, 1024);
     prof_begin(s);
-    zgemm_splitk_reduce<<<dim3(gx, (unsigned)nsplit), 256, 0, s>>>(d + total, nsplit);
+    launch_k(zgemm_splitk_reduce, dim3(gx, (unsigned)nsplit), 256, 0, s, d + total, nsplit);
     prof_end(s, "zgemm_reduce", 0.0, 0.0);
     count_launch();
   }

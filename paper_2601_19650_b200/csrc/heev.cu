@@ -533,6 +533,7 @@ __host__ __device__ inline size_t jac_warp_bytes(int n) {
 
 __global__ void __launch_bounds__(JAC_WARPS * 32) heev_jacobi(const HeevProblem* __restrict__ probs, int nprob,
                                                               int nmax) {
+  TCBC_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pi = blockIdx.x * JAC_WARPS + warp;
@@ -685,6 +686,7 @@ __global__ void __launch_bounds__(JAC_WARPS * 32) heev_jacobi(const HeevProblem*
 // ---------------------------------------------------------------- K1: tridiagonalisation
 template <int NQ>
 __global__ void __launch_bounds__(HEEV_THREADS, NQ == 4 ? 3 : 2) heev_tridiag(const HeevProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const HeevProblem P = probs[blockIdx.x];
   if (P.skip && *P.skip) return;   // exact-factor shortcut (chol_certify)
   const int n = P.n;
@@ -728,6 +730,7 @@ __host__ __device__ inline size_t cl_smem_bytes(int n, int cs) {
 
 template <int CS>
 __global__ void __launch_bounds__(CL_THREADS) heev_tridiag_cluster(const HeevProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
@@ -882,6 +885,7 @@ __device__ __forceinline__ double frcp(double b) {
 // 16384-eigenvalue levels: G = 4, ~17 rounds of 8 points, instead of 9 rounds of 64).
 template <int G>
 __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, int total) {
+  TCBC_PDL_WAIT();
   const int lane = threadIdx.x & 31, sub = lane % G;
   const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
   if ((blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / G >= total) return;   // whole warp idle
@@ -931,6 +935,7 @@ __global__ void heev_bisect(const HeevProblem* __restrict__ probs, int nprob, in
 
 // ---------------------------------------------------------------- K3: inverse iteration
 __global__ void heev_invit(const HeevProblem* __restrict__ probs, int nprob, int total) {
+  TCBC_PDL_WAIT();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= total) return;
   const HeevProblem& P = probs[find_estart(probs, nprob, g)];
@@ -1048,6 +1053,7 @@ constexpr size_t INVIT_SMEM_SHARED = 74u << 10;   // three blocks per SM when 8 
 
 __global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* __restrict__ probs, int nprob,
                                                             int total, int nmax) {
+  TCBC_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
   const int tl = threadIdx.x, NT = blockDim.x;
@@ -1155,6 +1161,7 @@ __global__ void __launch_bounds__(INVIT_NT) heev_invit_smem(const HeevProblem* _
 
 // ---------------------------------------------------------------- K4: CholeskyQR2 of Z
 __global__ void __launch_bounds__(HEEV_THREADS) heev_orth(const HeevProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const HeevProblem P = probs[blockIdx.x];
   if (P.skip && *P.skip) return;
   const int n = P.n, kmax = P.kmax, tid = threadIdx.x;
@@ -1213,6 +1220,7 @@ __host__ __device__ inline size_t orth_smem_bytes(int kmax) {
 }
 
 __global__ void __launch_bounds__(HEEV_THREADS) heev_orth_smem(const HeevProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const HeevProblem P = probs[blockIdx.x];
   if (P.skip && *P.skip) return;
   const int n = P.n, kmax = P.kmax, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1357,6 +1365,7 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_orth_smem(const HeevProblem
 
 // ---------------------------------------------------------------- K5: back-transform
 __global__ void heev_backtr(const HeevProblem* __restrict__ probs, int nprob, int total) {
+  TCBC_PDL_WAIT();
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= total) return;
   const HeevProblem& P = probs[find_estart(probs, nprob, gw)];
@@ -1406,6 +1415,7 @@ constexpr int WY_NB = 64;
 constexpr int WY_MIN_N = 96;   // below: the register / shared-memory kernel (fewer launches)
 
 __global__ void wy_prep(const HeevProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const HeevProblem P = probs[blockIdx.x];
   if (P.skip && *P.skip) return;
   const int n = P.n, kmax = P.kmax;
@@ -1433,6 +1443,7 @@ struct WyBlock {
 // one warp per block: T[c][c] = tau_c, T[r][c] = -tau_c sum_{r<=q<c} T[r][q] u_q,
 // u_q = (Y^H Y)[q][c] = conj(G[q][c])
 __global__ void wy_larft(const WyBlock* __restrict__ blks, int nb) {
+  TCBC_PDL_WAIT();
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (w >= nb) return;
   const WyBlock B = blks[w];
@@ -1464,6 +1475,7 @@ __global__ void wy_larft(const WyBlock* __restrict__ blks, int nb) {
 // what: 1 = the discarded weight (right after K6, so the host can read k and w early),
 // 2 = the eigenvalues (after inverse iteration, which shifts by the scaled values)
 __global__ void heev_unscale(const HeevProblem* __restrict__ probs, int nprob, int what) {
+  TCBC_PDL_WAIT();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nprob) return;
   const HeevProblem& P = probs[i];
@@ -1496,6 +1508,7 @@ __device__ __forceinline__ int find_bstart(const HeevProblem* p, int n, int b) {
 
 template <int NQ, int VPW>
 __global__ void __launch_bounds__(BT_WARPS * 32) heev_backtr_blk(const HeevProblem* __restrict__ probs, int nprob) {
+  TCBC_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const HeevProblem& P = probs[find_bstart(probs, nprob, blockIdx.x)];
@@ -1586,6 +1599,7 @@ __global__ void __launch_bounds__(BT_WARPS * 32) heev_backtr_blk(const HeevProbl
 
 // ---------------------------------------------------------------- K6: truncation decision
 __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
+  TCBC_PDL_WAIT();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nprob) return;
   const HeevProblem& P = probs[i];
@@ -1643,6 +1657,7 @@ __global__ void heev_finish(const HeevProblem* __restrict__ probs, int nprob) {
 // iteration, so the O(n) tridiagonal solves of a cluster run in parallel instead of one
 // after another.
 __global__ void __launch_bounds__(HEEV_THREADS) heev_invit_cluster(const HeevProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const HeevProblem P = probs[blockIdx.x];
   if (P.skip && *P.skip) return;
   const int n = P.n, kmax = P.kmax, tid = threadIdx.x;
@@ -1791,13 +1806,15 @@ void launch_cl(const HeevProblem* d, int nprob, size_t smem, cudaStream_t s) {
   cfg.blockDim = dim3(CL_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, heev_tridiag_cluster<CS>, d);
 }
 void launch_tridiag_cluster(const HeevProblem* d, int nprob, int cs, size_t smem, cudaStream_t s) {
@@ -1815,7 +1832,7 @@ namespace {
 // the WY back-transform of a launch (see wy_prep); Vt and A as in HeevProblem
 void backtr_wy(HeevProblem* h, int n, const HeevProblem* d, Stager& st, cudaStream_t s, Scratch* ws) {
   prof_begin(s);
-  wy_prep<<<n, 256, 0, s>>>(d);
+  launch_k(wy_prep, n, 256, 0, s, d);
   prof_end(s, "heev", 0.0, 0.0);
   count_launch();
   int maxb = 0;
@@ -1852,7 +1869,7 @@ void backtr_wy(HeevProblem* h, int n, const HeevProblem* d, Stager& st, cudaStre
   {
     const WyBlock* dw = static_cast<const WyBlock*>(st.put(wb.data(), sizeof(WyBlock) * wb.size()));
     prof_begin(s);
-    wy_larft<<<((int)wb.size() + 3) / 4, 128, 0, s>>>(dw, (int)wb.size());
+    launch_k(wy_larft, ((int)wb.size() + 3) / 4, 128, 0, s, dw, (int)wb.size());
     prof_end(s, "heev", 0.0, 0.0);
     count_launch();
   }
@@ -1904,7 +1921,7 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     double fl = 0.0;
     for (auto& p : small) fl += 8.0 * 8.0 * (double)p.n * p.n * p.n;   // ~8 sweeps of 8 n^3 flops
     prof_begin(s);
-    heev_jacobi<<<((int)small.size() + JAC_WARPS - 1) / JAC_WARPS, JAC_WARPS * 32, sm, s>>>(dj, (int)small.size(), nmax);
+    launch_k(heev_jacobi, ((int)small.size() + JAC_WARPS - 1) / JAC_WARPS, JAC_WARPS * 32, sm, s, dj, (int)small.size(), nmax);
     prof_end(s, "heev", fl, 32.0 * (double)small.size());
     count_launch();
   }
@@ -1963,9 +1980,9 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     const HeevProblem* dg = static_cast<const HeevProblem*>(st.put(g.data(), sizeof(HeevProblem) * g.size()));
     int mxn = 0;
     for (auto& p : g) mxn = std::max(mxn, p.n);
-    if (mxn <= 128) heev_tridiag<4><<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
-    else if (mxn <= 192) heev_tridiag<6><<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
-    else heev_tridiag<8><<<(int)g.size(), HEEV_THREADS, smem, s>>>(dg);
+    if (mxn <= 128) launch_k(heev_tridiag<4>, (int)g.size(), HEEV_THREADS, smem, s, dg);
+    else if (mxn <= 192) launch_k(heev_tridiag<6>, (int)g.size(), HEEV_THREADS, smem, s, dg);
+    else launch_k(heev_tridiag<8>, (int)g.size(), HEEV_THREADS, smem, s, dg);
     count_launch();
   }
   {   // smallest lanes-per-eigenvalue that still keeps ~6 warps per SM busy
@@ -1973,16 +1990,16 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     while (G < 32 && (long long)total * G < 148LL * 6 * 32) G *= 2;   // measured: 6 beats 3, 12, 24
     const int blocks = (int)(((long long)total * G + 255) / 256);
     switch (G) {
-      case 1: heev_bisect<1><<<blocks, 256, 0, s>>>(d, n, total); break;
-      case 2: heev_bisect<2><<<blocks, 256, 0, s>>>(d, n, total); break;
-      case 4: heev_bisect<4><<<blocks, 256, 0, s>>>(d, n, total); break;
-      case 8: heev_bisect<8><<<blocks, 256, 0, s>>>(d, n, total); break;
-      case 16: heev_bisect<16><<<blocks, 256, 0, s>>>(d, n, total); break;
-      default: heev_bisect<32><<<blocks, 256, 0, s>>>(d, n, total); break;
+      case 1: launch_k(heev_bisect<1>, blocks, 256, 0, s, d, n, total); break;
+      case 2: launch_k(heev_bisect<2>, blocks, 256, 0, s, d, n, total); break;
+      case 4: launch_k(heev_bisect<4>, blocks, 256, 0, s, d, n, total); break;
+      case 8: launch_k(heev_bisect<8>, blocks, 256, 0, s, d, n, total); break;
+      case 16: launch_k(heev_bisect<16>, blocks, 256, 0, s, d, n, total); break;
+      default: launch_k(heev_bisect<32>, blocks, 256, 0, s, d, n, total); break;
     }
   }
-  heev_finish<<<(n + 127) / 128, 128, 0, s>>>(d, n);   // k and w: only kept pairs go on
-  heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n, 1);
+  launch_k(heev_finish, (n + 127) / 128, 128, 0, s, d, n);   // k and w: only kept pairs go on
+  launch_k(heev_unscale, (n + 127) / 128, 128, 0, s, d, n, 1);
   if (values_ready) values_ready();   // k and w are final: the caller may read them now
   {
     int mxn = 1;
@@ -1995,21 +2012,21 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     const size_t ism = (size_t)6 * mxn * nt * sizeof(double);
     if (ism <= INVIT_SMEM_MAX) {
       func_smem(heev_invit_smem, INVIT_SMEM_MAX);
-      heev_invit_smem<<<(total + nt - 1) / nt, nt, ism, s>>>(d, n, total, mxn);
+      launch_k(heev_invit_smem, (total + nt - 1) / nt, nt, ism, s, d, n, total, mxn);
     } else {
-      heev_invit<<<(total + 127) / 128, 128, 0, s>>>(d, n, total);
+      launch_k(heev_invit, (total + 127) / 128, 128, 0, s, d, n, total);
     }
   }
-  heev_invit_cluster<<<n, HEEV_THREADS, 0, s>>>(d);
+  launch_k(heev_invit_cluster, n, HEEV_THREADS, 0, s, d);
   count_launch();
   {
     int mk = 0;
     for (int i = 0; i < n; ++i) mk = std::max(mk, h[i].kmax);
     if (mk <= ORTH_SMEM_K) {
       func_smem(heev_orth_smem, orth_smem_bytes(ORTH_SMEM_K));
-      heev_orth_smem<<<n, HEEV_THREADS, orth_smem_bytes(mk), s>>>(d);
+      launch_k(heev_orth_smem, n, HEEV_THREADS, orth_smem_bytes(mk), s, d);
     } else {
-      heev_orth<<<n, HEEV_THREADS, 0, s>>>(d);
+      launch_k(heev_orth, n, HEEV_THREADS, 0, s, d);
     }
   }
   int mxn_all = 0;
@@ -2023,7 +2040,7 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     count_launch(); count_launch(); count_launch(); count_launch(); count_launch();   // K2, K6, K7, K3, K4
     backtr_wy(h, n, d, st, s, ws);
     prof_begin(s);
-    heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n, 2);
+    launch_k(heev_unscale, (n + 127) / 128, 128, 0, s, d, n, 2);
     prof_end(s, "heev", 0.0, 0.0);
     count_launch();
     return;
@@ -2035,14 +2052,14 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
       func_smem(heev_backtr_blk<4, BT_VPW>, backtr_smem_bytes(256));
       func_smem(heev_backtr_blk<6, BT_VPW>, backtr_smem_bytes(256));
       func_smem(heev_backtr_blk<8, BT_VPW>, backtr_smem_bytes(256));
-      if (mxn <= 128) heev_backtr_blk<4, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
-      else if (mxn <= 192) heev_backtr_blk<6, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
-      else heev_backtr_blk<8, BT_VPW><<<nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s>>>(d, n);
+      if (mxn <= 128) launch_k(heev_backtr_blk<4, BT_VPW>, nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s, d, n);
+      else if (mxn <= 192) launch_k(heev_backtr_blk<6, BT_VPW>, nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s, d, n);
+      else launch_k(heev_backtr_blk<8, BT_VPW>, nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s, d, n);
     } else {
-      heev_backtr<<<(total * 32 + 255) / 256, 256, 0, s>>>(d, n, total);
+      launch_k(heev_backtr, (total * 32 + 255) / 256, 256, 0, s, d, n, total);
     }
   }
-  heev_unscale<<<(n + 127) / 128, 128, 0, s>>>(d, n, 2);
+  launch_k(heev_unscale, (n + 127) / 128, 128, 0, s, d, n, 2);
   count_launch();
   count_launch();
   count_launch(); count_launch(); count_launch(); count_launch(); count_launch();

@@ -3,11 +3,35 @@
 // (what the kernel reads); both describe the same problems.
 #pragma once
 #include <functional>
+#include <utility>
 #include <vector>
 #include <cuda_runtime.h>
 #include <cstdint>
 
 namespace tcbc {
+
+// Programmatic dependent launch (sm_90+): every kernel of the library begins with
+// griddepcontrol.wait (it returns once the preceding grid of the stream has completed and its
+// writes are visible; immediately when there is none), so launching with
+// cudaLaunchAttributeProgrammaticStreamSerialization only lets a kernel's launch and prologue
+// overlap the tail of the previous one.  No kernel triggers its dependents early (a persistent
+// GEMM must keep every SM).  TTN_NO_PDL=1 launches without the attribute.
+#define TCBC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 typedef double2 cplx;   // (x = re, y = im), 16-byte aligned
 

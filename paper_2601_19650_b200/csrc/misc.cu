@@ -19,6 +19,11 @@ long long launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
 void add_launches(long long delta) { g_launches.fetch_add(delta); }
 
+bool pdl_enabled() {
+  static const bool on = getenv("TTN_NO_PDL") == nullptr;
+  return on;
+}
+
 void func_attr(const void* func, cudaFuncAttribute attr, int value) {
   static std::mutex mu;
   static std::map<std::tuple<int, const void*, int>, int> set;
@@ -45,6 +50,7 @@ __device__ __forceinline__ int find_by_start(const P* p, int n, long long idx) {
 }
 
 __global__ void permute_grouped(const PermProblem* __restrict__ probs, int nprob, long long total) {
+  TCBC_PDL_WAIT();
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x) {
     int pi = find_by_start(probs, nprob, g);
@@ -64,6 +70,7 @@ __global__ void permute_grouped(const PermProblem* __restrict__ probs, int nprob
 }
 
 __global__ void scale_rows_grouped(const ScaleRowsProblem* __restrict__ probs, int nprob, long long total) {
+  TCBC_PDL_WAIT();
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x) {
     int pi = find_by_start(probs, nprob, g);
@@ -77,6 +84,7 @@ __global__ void scale_rows_grouped(const ScaleRowsProblem* __restrict__ probs, i
 }
 
 __global__ void sumsq_kernel(const SumsqProblem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const SumsqProblem P = probs[blockIdx.x];
   double acc = 0.0;
   for (long long i = threadIdx.x; i < P.len; i += blockDim.x) {
@@ -95,6 +103,7 @@ __global__ void sumsq_kernel(const SumsqProblem* __restrict__ probs) {
 }
 
 __global__ void eye_grouped(const EyeProblem* __restrict__ probs, int nprob, long long total) {
+  TCBC_PDL_WAIT();
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x) {
     int pi = find_by_start(probs, nprob, g);
@@ -106,6 +115,7 @@ __global__ void eye_grouped(const EyeProblem* __restrict__ probs, int nprob, lon
 }
 
 __global__ void fill_kernel(cplx* p, long long n, cplx v) {
+  TCBC_PDL_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = v;
 }
@@ -116,6 +126,7 @@ int grid_for(long long total, int threads) {
 }
 
 __global__ void pow2_maxexp(const Pow2Problem* __restrict__ probs) {
+  TCBC_PDL_WAIT();
   const Pow2Problem& P = probs[blockIdx.y];
   int e = -2147483000;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.len; i += (long long)gridDim.x * blockDim.x) {
@@ -128,6 +139,7 @@ __global__ void pow2_maxexp(const Pow2Problem* __restrict__ probs) {
 }
 
 __global__ void pow2_scale(const Pow2Problem* __restrict__ probs, int sign) {
+  TCBC_PDL_WAIT();
   const Pow2Problem& P = probs[blockIdx.y];
   const int e = pow2_effective(*P.exp);
   if (e == 0) return;
@@ -141,6 +153,7 @@ __global__ void pow2_scale(const Pow2Problem* __restrict__ probs, int sign) {
 }
 
 __global__ void spec_check(const SpecCheck* __restrict__ p, int n, double* wacc, int* xacc, int* flag) {
+  TCBC_PDL_WAIT();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const SpecCheck c = p[j];
@@ -154,6 +167,7 @@ __global__ void spec_check(const SpecCheck* __restrict__ p, int n, double* wacc,
 }
 
 __global__ void flag_nonzero(const int* info, int n, int* flag, int bit) {
+  TCBC_PDL_WAIT();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n && info[j] != 0) atomicOr(flag, bit);
 }
@@ -163,13 +177,13 @@ __global__ void flag_nonzero(const int* info, int n, int* flag, int bit) {
 void launch_spec_check(SpecCheck* h, int n, double* wacc, int* xacc, int* flag, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   const SpecCheck* d = static_cast<const SpecCheck*>(st.put(h, sizeof(SpecCheck) * n));
-  spec_check<<<(n + 127) / 128, 128, 0, s>>>(d, n, wacc, xacc, flag);
+  launch_k(spec_check, (n + 127) / 128, 128, 0, s, d, n, wacc, xacc, flag);
   count_launch();
 }
 
 void launch_flag_nonzero(const int* info, int n, int* flag, int bit, cudaStream_t s) {
   if (n == 0) return;
-  flag_nonzero<<<(n + 127) / 128, 128, 0, s>>>(info, n, flag, bit);
+  launch_k(flag_nonzero, (n + 127) / 128, 128, 0, s, info, n, flag, bit);
   count_launch();
 }
 
@@ -185,7 +199,7 @@ void launch_permute(PermProblem* h, int n, Stager& st, cudaStream_t s) {
     fprintf(stderr, "\n");
   }
   prof_begin(s);
-  permute_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  launch_k(permute_grouped, grid_for(total, 256), 256, 0, s, d, n, total);
   prof_end(s, "permute", 0.0, 32.0 * (double)total);
   count_launch();
 }
@@ -196,7 +210,7 @@ void launch_scale_rows(ScaleRowsProblem* h, int n, Stager& st, cudaStream_t s) {
   if (total == 0) return;
   const ScaleRowsProblem* d = static_cast<const ScaleRowsProblem*>(st.put(h, sizeof(ScaleRowsProblem) * n));
   prof_begin(s);
-  scale_rows_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  launch_k(scale_rows_grouped, grid_for(total, 256), 256, 0, s, d, n, total);
   prof_end(s, "scale_rows", 0.0, 32.0 * (double)total);
   count_launch();
 }
@@ -205,7 +219,7 @@ void launch_sumsq(SumsqProblem* h, int n, Stager& st, cudaStream_t s) {
   if (n == 0) return;
   const SumsqProblem* d = static_cast<const SumsqProblem*>(st.put(h, sizeof(SumsqProblem) * n));
   prof_begin(s);
-  sumsq_kernel<<<n, 256, 0, s>>>(d);
+  launch_k(sumsq_kernel, n, 256, 0, s, d);
   prof_end(s, "misc", 0.0, 0.0);
   count_launch();
 }
@@ -216,7 +230,7 @@ void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s) {
   if (total == 0) return;
   const EyeProblem* d = static_cast<const EyeProblem*>(st.put(h, sizeof(EyeProblem) * n));
   prof_begin(s);
-  eye_grouped<<<grid_for(total, 256), 256, 0, s>>>(d, n, total);
+  launch_k(eye_grouped, grid_for(total, 256), 256, 0, s, d, n, total);
   prof_end(s, "misc", 0.0, 16.0 * (double)total);
   count_launch();
 }
@@ -224,7 +238,7 @@ void launch_eye(EyeProblem* h, int n, Stager& st, cudaStream_t s) {
 void launch_fill(cplx* p, long long n, cplx v, cudaStream_t s) {
   if (n <= 0) return;
   prof_begin(s);
-  fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
+  launch_k(fill_kernel, grid_for(n, 256), 256, 0, s, p, n, v);
   prof_end(s, "misc", 0.0, 16.0 * (double)n);
   count_launch();
 }
@@ -250,8 +264,8 @@ void launch_pow2_normalize(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
     for (int i = 0; i < n; ++i) cudaMemsetAsync(h[i].exp, 0x80, sizeof(int), s);
   const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
   const unsigned gx = (unsigned)std::min<long long>((mx + 255) / 256, 296);
-  pow2_maxexp<<<dim3(gx, n), 256, 0, s>>>(d);
-  pow2_scale<<<dim3(pow2_gx(mx, n), n), 256, 0, s>>>(d, -1);
+  launch_k(pow2_maxexp, dim3(gx, n), 256, 0, s, d);
+  launch_k(pow2_scale, dim3(pow2_gx(mx, n), n), 256, 0, s, d, -1);
   count_launch();
   count_launch();
 }
@@ -261,7 +275,7 @@ void launch_pow2_restore(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
   long long mx = 1;
   for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].len);
   const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
-  pow2_scale<<<dim3(pow2_gx(mx, n), n), 256, 0, s>>>(d, +1);
+  launch_k(pow2_scale, dim3(pow2_gx(mx, n), n), 256, 0, s, d, +1);
   count_launch();
 }
 
@@ -270,7 +284,7 @@ void launch_pow2_apply(Pow2Problem* h, int n, Stager& st, cudaStream_t s) {
   long long mx = 1;
   for (int i = 0; i < n; ++i) mx = std::max(mx, h[i].len);
   const Pow2Problem* d = static_cast<const Pow2Problem*>(st.put(h, sizeof(Pow2Problem) * n));
-  pow2_scale<<<dim3(pow2_gx(mx, n), n), 256, 0, s>>>(d, -1);
+  launch_k(pow2_scale, dim3(pow2_gx(mx, n), n), 256, 0, s, d, -1);
   count_launch();
 }
 
