@@ -15,7 +15,8 @@ namespace tcbc {
 // writes are visible; immediately when there is none), so launching with
 // cudaLaunchAttributeProgrammaticStreamSerialization only lets a kernel's launch and prologue
 // overlap the tail of the previous one.  No kernel triggers its dependents early (a persistent
-// GEMM must keep every SM).  TTN_NO_PDL=1 launches without the attribute.
+// GEMM must keep every SM).  Opt-in (TTN_PDL=1): measured neutral to slightly negative on
+// configs 1, 2, 3 and 5 (the small kernels' own duration, not the launch gap, dominates).
 #define TCBC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>

@@ -19,8 +19,8 @@ long long launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
 void add_launches(long long delta) { g_launches.fetch_add(delta); }
 
-bool pdl_enabled() {
-  static const bool on = getenv("TTN_NO_PDL") == nullptr;
+bool pdl_enabled() {   // measured neutral-to-negative on configs 1, 2, 3, 5: opt-in
+  static const bool on = getenv("TTN_PDL") != nullptr;
   return on;
 }
 
