@@ -155,7 +155,7 @@ __host__ __device__ inline int fused_r0(int n) {
 // memory (r0 = 0: all of it), rows < r0 in the global A.
 // Reflector j is written to row j (columns > j) of the global A for the back-transform.
 // NQ: 32-column blocks per row (n <= 32 NQ).
-template <int NQ, bool PAIR>
+template <int NQ>
 __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, cplx* vcur, cplx* wcur, cplx* base,
                               double* dvec, double* evec, cplx* tau_out, double2* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -238,25 +238,17 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
     for (int q = 0; q < NQ; ++q) cacc[q] = make_double2(0.0, 0.0);
     // the row's contribution (update of U_{j-1}, its dot with v_j, the column partials) without
     // the cross-lane reduction of the dot
-    // a row's entries (shared-memory tail or global), as one generic pointer: no per-entry
-    // branch; entries past the diagonal are masked by selects, not branches
-    auto row_ptr = [&](const int r) -> cplx* {
-      return r >= r0 ? Ap + ((size_t)r * (r + 1) / 2 - pbase) : A + (size_t)r * n;
-    };
-    auto row_load = [&](const int r, cplx (&a)[NQ]) {
+    auto row_partial = [&](const int r, double& sr, double& si) {
       const int nq = (r - j + 31) >> 5;   // column blocks that reach the diagonal (warp-uniform)
-      const cplx* rowp = row_ptr(r);
+      // the row's storage (shared-memory tail or global), as one generic pointer: no per-entry
+      // branch; entries past the diagonal are masked by selects, not branches
+      cplx* rowp = r >= r0 ? Ap + ((size_t)r * (r + 1) / 2 - pbase) : A + (size_t)r * n;
+      cplx a[NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int c = j + 1 + lane + 32 * q;
         a[q] = (q < nq && c <= r) ? rowp[c] : make_double2(0.0, 0.0);
       }
-    };
-    // the row's contribution (update of U_{j-1}, its dot with v_j, the column partials) from
-    // its loaded entries, without the cross-lane reduction of the dot
-    auto row_compute = [&](const int r, cplx (&a)[NQ], double& sr, double& si) {
-      const int nq = (r - j + 31) >> 5;
-      cplx* rowp = row_ptr(r);
       const cplx vr = vcur[r];
       const cplx vpr = vprev[r], wpr = wprev[r];
 #pragma unroll
@@ -289,11 +281,6 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
         cacc[q].y = fma(av.x, wy, fma(-av.y, wx, cacc[q].y));
       }
     };
-    auto row_partial = [&](const int r, double& sr, double& si) {
-      cplx a[NQ];
-      row_load(r, a);
-      row_compute(r, a, sr, si);
-    };
     if constexpr (NQ <= 6) {
       // R rows per reduction (4 for n <= 128, 2 for n <= 192, as registers allow): their 2R
       // lane-partials (re, im) are summed over the warp by a transposing butterfly (2R + 1
@@ -302,34 +289,13 @@ __device__ void tridiag_fused(cplx* __restrict__ A, const int n, const int r0, c
       constexpr int R = NQ <= 4 ? 4 : 2;
       for (int rb = j + 1 + warp; rb < n; rb += R * HEEV_WARPS) {
         double v[2 * R];
-        // rows in pairs with both pairs' loads issued before either is updated: the update's
-        // stores could alias the next row's loads, so without the hoist the compiler serialises
-        // one global / L2 round trip per row
-        if constexpr (!PAIR) {
 #pragma unroll
-          for (int u = 0; u < R; ++u) {
-            const int r = rb + u * HEEV_WARPS;
-            double sr = 0.0, si = 0.0;
-            if (r < n) row_partial(r, sr, si);
-            v[2 * u] = sr;
-            v[2 * u + 1] = si;
-          }
-        } else
-#pragma unroll
-        for (int u = 0; u < R; u += 2) {
-          const int r0_ = rb + u * HEEV_WARPS, r1_ = rb + (u + 1) * HEEV_WARPS;
-          cplx a0[NQ], a1[NQ];
-          if (r0_ < n) row_load(r0_, a0);
-          if (r1_ < n) row_load(r1_, a1);
+        for (int u = 0; u < R; ++u) {
+          const int r = rb + u * HEEV_WARPS;
           double sr = 0.0, si = 0.0;
-          if (r0_ < n) row_compute(r0_, a0, sr, si);
+          if (r < n) row_partial(r, sr, si);
           v[2 * u] = sr;
           v[2 * u + 1] = si;
-          sr = 0.0;
-          si = 0.0;
-          if (r1_ < n) row_compute(r1_, a1, sr, si);
-          v[2 * u + 2] = sr;
-          v[2 * u + 3] = si;
         }
         // halve the value count per round: lanes with the round's bit set keep the upper half
         int idx = 0;
@@ -718,7 +684,7 @@ __global__ void __launch_bounds__(JAC_WARPS * 32) heev_jacobi(const HeevProblem*
 }
 
 // ---------------------------------------------------------------- K1: tridiagonalisation
-template <int NQ, bool PAIR>
+template <int NQ>
 __global__ void __launch_bounds__(HEEV_THREADS, NQ == 4 ? 3 : 2) heev_tridiag(const HeevProblem* __restrict__ probs) {
   TCBC_PDL_WAIT();
   const HeevProblem P = probs[blockIdx.x];
@@ -737,10 +703,10 @@ __global__ void __launch_bounds__(HEEV_THREADS, NQ == 4 ? 3 : 2) heev_tridiag(co
   for (int i = tid; i < n; i += HEEV_THREADS) tr += A[(size_t)i * n + i].x;
   const double trace = block_sum2(tr, 0.0, red).x;
   if constexpr (NQ == 8) {   // the launcher sends n > 192 only to this instantiation
-    if (n <= 32 * NQ) tridiag_fused<NQ, PAIR>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
+    if (n <= 32 * NQ) tridiag_fused<NQ>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
     else tridiag_full(A, n, sv, sp, dvec, evec, P.tau, red);
   } else {
-    tridiag_fused<NQ, PAIR>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
+    tridiag_fused<NQ>(A, n, fused_r0(n), sv, sp, base, dvec, evec, P.tau, red);
   }
   tridiag_stats(P, trace);
 }
@@ -1965,14 +1931,9 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
   }
   HeevProblem* h = rest.data();
   const int n = (int)rest.size();
-  // rows loaded in pairs before either is updated (PAIR): measured per order (A/B knobs)
-  static const bool pair4 = getenv("TTN_TRIDIAG_PAIR4") != nullptr;
-  static const bool pair6 = getenv("TTN_TRIDIAG_NOPAIR6") == nullptr;
-  func_smem(heev_tridiag<4, false>, FUSED_SMEM_BUDGET);
-  func_smem(heev_tridiag<4, true>, FUSED_SMEM_BUDGET);
-  func_smem(heev_tridiag<6, false>, FUSED_SMEM_BUDGET);
-  func_smem(heev_tridiag<6, true>, FUSED_SMEM_BUDGET);
-  func_smem(heev_tridiag<8, false>, FUSED_SMEM_BUDGET);
+  func_smem(heev_tridiag<4>, FUSED_SMEM_BUDGET);
+  func_smem(heev_tridiag<6>, FUSED_SMEM_BUDGET);
+  func_smem(heev_tridiag<8>, FUSED_SMEM_BUDGET);
   int total = 0;
   double fl = 0.0, by = 0.0;
   int nblk = 0;
@@ -2019,15 +1980,9 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     const HeevProblem* dg = static_cast<const HeevProblem*>(st.put(g.data(), sizeof(HeevProblem) * g.size()));
     int mxn = 0;
     for (auto& p : g) mxn = std::max(mxn, p.n);
-    if (mxn <= 128) {
-      if (pair4) launch_k(heev_tridiag<4, true>, (int)g.size(), HEEV_THREADS, smem, s, dg);
-      else launch_k(heev_tridiag<4, false>, (int)g.size(), HEEV_THREADS, smem, s, dg);
-    } else if (mxn <= 192) {
-      if (pair6) launch_k(heev_tridiag<6, true>, (int)g.size(), HEEV_THREADS, smem, s, dg);
-      else launch_k(heev_tridiag<6, false>, (int)g.size(), HEEV_THREADS, smem, s, dg);
-    } else {
-      launch_k(heev_tridiag<8, false>, (int)g.size(), HEEV_THREADS, smem, s, dg);
-    }
+    if (mxn <= 128) launch_k(heev_tridiag<4>, (int)g.size(), HEEV_THREADS, smem, s, dg);
+    else if (mxn <= 192) launch_k(heev_tridiag<6>, (int)g.size(), HEEV_THREADS, smem, s, dg);
+    else launch_k(heev_tridiag<8>, (int)g.size(), HEEV_THREADS, smem, s, dg);
     count_launch();
   }
   {   // smallest lanes-per-eigenvalue that still keeps ~6 warps per SM busy
