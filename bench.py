@@ -513,10 +513,10 @@ def run_native(args, rank, world, local_rank):
     # DRAM traffic of the zgemm launches of one step of this config (committed ncu capture),
     # per profiler launch (one launch_gemm call: its variant kernels back to back) like `achieved`
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"ncu_zgemm_traffic_r01_c{cfg}.json")
+    tp = os.path.join(ROOT, "profiles", f"ncu_zgemm_traffic_r02_c{cfg}.json")
     if os.path.exists(tp) and g["launches"]:
         try:
-            traffic = json.load(open(tp))["bytes_per_step"] / (g["launches"] / args.steps)
+            traffic = json.load(open(tp))["bytes_per_step"] / (g["launches"] / prof_steps)
         except Exception:
             traffic = None
     value = applies_all / (ms_max / 1000.0)
@@ -562,7 +562,7 @@ def run_native(args, rank, world, local_rank):
                      "flops_per_launch": g["flops"] / max(g["launches"], 1),
                      "algorithmic_bytes_per_launch": g["bytes"] / max(g["launches"], 1),
                      "ms_per_launch": g["ms"] / max(g["launches"], 1),
-                     "traffic_source": f"profiles/ncu_zgemm_traffic_r01_c{cfg}.json: DRAM read+write of every "
+                     "traffic_source": f"profiles/ncu_zgemm_traffic_r02_c{cfg}.json: DRAM read+write of every "
                                        "zgemm_grouped kernel of one step (ncu, cold-cache replays) / launch sets per step"},
         "kernels": kern,
         "gpu_launches": int(launches),

@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <functional>
 #include <stdexcept>
 #include <string>
@@ -99,7 +100,7 @@ struct ttn_ctx_s : tcbc::MemSource {
   std::string last_error;
   // level-synchronous schedule options (ttn_ctx_set_schedule): speculative ranks (no host
   // synchronisation inside an apply) and CUDA-graph replay of speculative applies
-  bool speculate = true;
+  bool speculate = getenv("TTN_NO_SPECULATE") == nullptr;   // (A/B knob; ttn_ctx_set_schedule)
   bool graphs = true;
   bool capturing = false;        // a graph capture is in progress on this ctx (no arena growth)
   tcbc::GraphCache* gr = nullptr;          // graph cache and the shapes whose speculation failed
