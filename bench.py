@@ -447,8 +447,9 @@ def run_native(args, rank, world, local_rank):
             for h in st_h + op_h + outs:
                 h.destroy()
 
-        for lane in lanes:   # warm-up (untimed)
-            e2e_step(lane)
+        for lane in lanes:   # warm-up (untimed): the second apply of a shape may capture its CUDA graph
+            for _ in range(2):
+                e2e_step(lane)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

@@ -252,6 +252,22 @@ TTN_API ttn_status ttn_profile_read(const char* family, double* ms, double* flop
 /* Number of kernels this library has launched in this process.                           */
 TTN_API ttn_status ttn_launch_count(int64_t* out);
 
+/* ---------------------------------------------------------------- eigensolver test hook */
+/* The compress step's batched Hermitian eigensolver (B:5 (c); the truncation of
+ * P:119, "compressed down to the desired new bond dimension", with the tolerance of P:362) on
+ * nmat host matrices, for tests: a_host holds nmat n x n Hermitian matrices (row-major, full
+ * storage, consecutive); on return lam_host[i*kmax + t] are the kmax largest eigenvalues of
+ * matrix i (descending; entries past the kept rank are 0), vt_host[(i*kmax + t)*n + j] the
+ * j-th entry of eigenvector t (rows past the kept rank are 0), k_host[i] the kept rank
+ * k = min(max_bond, #{lam > tol^2 lam_1}, #{lam > 1e-13 lam_1}) >= 1 and w_host[i] the
+ * discarded weight trace - sum_{t<k} lam_t.  route: 0 = the library's choice, 1 = one-stage
+ * tridiagonalisation, 2 = two-stage (band) reduction wherever 65 <= n <= 256.  Host buffers
+ * are the caller's; synchronises.  Errors: ARG (sizes, kmax > n, tol outside [0, 1), route),
+ * UNSUPPORTED (n beyond the eigensolver), CUDA.                                           */
+TTN_API ttn_status ttn_test_heev(ttn_ctx ctx, int32_t nmat, int32_t n, int32_t kmax, int32_t max_bond, double tol,
+                                 int32_t route, const ttn_c128* a_host, double* lam_host, ttn_c128* vt_host,
+                                 int32_t* k_host, double* w_host);
+
 /* ||a|| = sqrt(Re <a|a>) (ttn_overlap of a with itself; Eq. 2, used to normalise the
  * initial state, reading A16, and as ||phi|| in the report).  Synchronises.
  * Errors: ARG, TOPOLOGY.                                                                  */

@@ -275,6 +275,26 @@ def ttn_launch_count() -> int:
     return v.value
 
 
+def ttn_test_heev(ctx: Context, a: np.ndarray, kmax: int, max_bond: int | None = None, tol: float = 0.0,
+                  route: int = 0):
+    """The compress eigensolver on host matrices a[nmat, n, n] (test hook, include/ttn_cbc.h):
+    returns (lam[nmat, kmax], vt[nmat, kmax, n], k[nmat], w[nmat])."""
+    a = L.host_c128(a)
+    if a.ndim == 2:
+        a = a[None]
+    nmat, n, n2 = a.shape
+    if n != n2:
+        raise ValueError("square matrices expected")
+    mb = kmax if max_bond is None else max_bond
+    lam = np.zeros((nmat, kmax))
+    vt = np.zeros((nmat, kmax, n), np.complex128)
+    k = np.zeros(nmat, np.int32)
+    w = np.zeros(nmat)
+    L.check(ctx.h, L.load().ttn_test_heev(ctx.h, nmat, n, kmax, mb, float(tol), route, a.ctypes.data,
+                                          lam.ctypes.data, vt.ctypes.data, k.ctypes.data, w.ctypes.data))
+    return lam, vt, k, w
+
+
 def ttn_norm(ctx: Context, a: TTN) -> float:
     v = C.c_double()
     L.check(ctx.h, L.load().ttn_norm(ctx.h, a.h, C.byref(v)))

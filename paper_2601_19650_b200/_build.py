@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libttncbc.so")
-SOURCES = ["gemm.cu", "heev.cu", "chfsi.cu", "chol.cu", "misc.cu", "prof.cpp", "comm.cpp", "contract.cpp", "cbc.cpp", "runtime.cpp", "api.cpp"]
+SOURCES = ["gemm.cu", "heev.cu", "heev2s.cu", "chfsi.cu", "chol.cu", "misc.cu", "prof.cpp", "comm.cpp", "contract.cpp", "cbc.cpp", "runtime.cpp", "api.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]

@@ -23,7 +23,7 @@ SYMBOLS = ["ttn_ctx_create", "ttn_ctx_destroy", "ttn_last_error", "ttn_version",
            "ttn_overlap_batch", "ttn_norm", "ttn_get_data", "ttn_get_data_batch", "ttn_profile_enable", "ttn_profile_read", "ttn_launch_count",
            "ttn_comm_unique_id", "ttn_ctx_set_comm", "ttn_partition_plan", "ttn_ctx_set_workers",
            "ttn_sandwich", "ttn_op_norm2", "ttn_ctx_set_schedule",
-           "ttn_loopback_create", "ttn_loopback_destroy", "ttn_ctx_set_comm_loopback"]
+           "ttn_loopback_create", "ttn_loopback_destroy", "ttn_ctx_set_comm_loopback", "ttn_test_heev"]
 
 
 class c128(C.Structure):
@@ -98,6 +98,7 @@ def load():
         "ttn_op_norm2": (C.c_int, [P, P, P, C.POINTER(D)]),
         "ttn_ctx_set_comm": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int]),
         "ttn_partition_plan": (C.c_int, [I32, C.POINTER(I32), C.c_int, C.POINTER(I32)]),
+        "ttn_test_heev": (C.c_int, [P, I32, I32, I32, I32, D, I32, P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -2,6 +2,7 @@
 // exceptions to a ttn_status and records the message on the context.
 #include "prof.h"
 #include "runtime.h"
+#include "heev2s.h"
 
 #include <cmath>
 #include <cstring>
@@ -365,6 +366,59 @@ ttn_status ttn_op_norm2(ttn_ctx ctx, ttn op, ttn ket, double* out) {
     cplx r;
     sweep_impl(ctx, 1, L, &r);
     *out = r.x;
+  });
+}
+
+ttn_status ttn_test_heev(ttn_ctx ctx, int32_t nmat, int32_t n, int32_t kmax, int32_t max_bond, double tol,
+                         int32_t route, const ttn_c128* a_host, double* lam_host, ttn_c128* vt_host,
+                         int32_t* k_host, double* w_host) {
+  if (!ctx || nmat < 1 || n < 1 || kmax < 1 || kmax > n || max_bond < 1 || !(tol >= 0.0 && tol < 1.0) || !a_host ||
+      !lam_host || !vt_host || !k_host || !w_host || route < 0 || route > 2)
+    return TTN_ERR_ARG;
+  DeviceGuard g(ctx->device);
+  return guard(ctx, [&] {
+    if (n > tcbc::heev_max_n()) throw Error(TTN_ERR_UNSUPPORTED, "ttn_test_heev: order beyond the eigensolver");
+    using tcbc::cplx;
+    const size_t nn = (size_t)n * n;
+    cplx* dA = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * nn * nmat));
+    double* dlam = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * (size_t)kmax * nmat));
+    cplx* dVt = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * (size_t)kmax * n * nmat));
+    int* dk = static_cast<int*>(ctx->scratch.alloc(sizeof(int) * nmat));
+    double* dw = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * nmat));
+    TTN_CUDA(cudaMemcpyAsync(dA, a_host, sizeof(cplx) * nn * nmat, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<tcbc::HeevProblem> hp(nmat);
+    for (int i = 0; i < nmat; ++i) {
+      tcbc::HeevProblem& h = hp[i];
+      h = tcbc::HeevProblem{};
+      h.A = dA + nn * i;
+      h.n = n;
+      h.kmax = kmax;
+      h.lam = dlam + (size_t)kmax * i;
+      h.Vt = dVt + (size_t)kmax * n * i;
+      h.k_out = dk + i;
+      h.w_out = dw + i;
+      h.work = static_cast<double*>(ctx->scratch.alloc(sizeof(double) * tcbc::heev_work_doubles(n, kmax)));
+      h.tau = static_cast<cplx*>(ctx->scratch.alloc(sizeof(cplx) * n));
+      h.tol2 = tol * tol;
+      h.floor_rel = 1e-13;
+      h.max_bond = max_bond;
+    }
+    tcbc::heev2s_set_route(route);
+    try {
+      tcbc::launch_heev(hp.data(), nmat, *ctx->stager, ctx->stream);
+    } catch (...) {
+      tcbc::heev2s_set_route(0);
+      throw;
+    }
+    tcbc::heev2s_set_route(0);
+    TTN_CUDA(cudaGetLastError());
+    TTN_CUDA(cudaMemcpyAsync(lam_host, dlam, sizeof(double) * (size_t)kmax * nmat, cudaMemcpyDeviceToHost, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(vt_host, dVt, sizeof(cplx) * (size_t)kmax * n * nmat, cudaMemcpyDeviceToHost, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(k_host, dk, sizeof(int) * nmat, cudaMemcpyDeviceToHost, ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(w_host, dw, sizeof(double) * nmat, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    TTN_CUDA(cudaGetLastError());
+    ctx->scratch.reset();
   });
 }
 

@@ -22,6 +22,7 @@
 //              >= 1 and discarded weight w = trace(A) - sum_{t<k} lam_t.
 #include "kernels.h"
 #include "prof.h"
+#include "heev2s.h"
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cfloat>
@@ -1781,8 +1782,8 @@ __global__ void __launch_bounds__(HEEV_THREADS) heev_invit_cluster(const HeevPro
 }  // namespace
 
 size_t heev_work_doubles(int n, int kmax) {
-  return (size_t)2 * n + 8 + (size_t)n * kmax * 6 + (size_t)kmax * kmax + 2 * (size_t)kmax +
-         (size_t)HEEV_WARPS * 6 * n;
+  static_assert(HEEV_WARPS == 8 && S_TRACE == H2S_S_TRACE, "heev2s.h mirrors this layout");
+  return heev_base_doubles(n, kmax) + h2s_extra_doubles(n);
 }
 
 size_t heev_smem_bytes(int n, int kmax) {
@@ -1969,9 +1970,23 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
       count_launch();
     }
   }
+  // two-stage reduction (heev2s.cu) for the one-CTA Grams of order 65..256
+  std::vector<char> is2s(n, 0);
+  std::vector<HeevProblem> p2s;
+  int maxn2s = 0;
   for (int i = 0; i < n; ++i) {
     if (!cgrp.empty() && h[i].n > 96) continue;
+    if (heev2s_use(h[i].n, n)) {
+      is2s[i] = 1;
+      p2s.push_back(h[i]);
+      maxn2s = std::max(maxn2s, h[i].n);
+      continue;
+    }
     grp[h[i].n <= SMEM_MAX_N ? 0 : (h[i].n <= FUSED_MAX_N ? 1 : 2)].push_back(h[i]);
+  }
+  if (!p2s.empty()) {
+    const HeevProblem* d2 = static_cast<const HeevProblem*>(st.put(p2s.data(), sizeof(HeevProblem) * p2s.size()));
+    launch_heev2s_reduce(d2, (int)p2s.size(), maxn2s, s);
   }
   for (auto& g : grp) {
     if (g.empty()) continue;
@@ -2045,18 +2060,40 @@ void launch_heev(HeevProblem* hin, int nin, Stager& st, cudaStream_t s, const st
     count_launch();
     return;
   }
-  {
+  const HeevProblem* dbt = d;   // the one-stage back-transform's problems
+  int nbt = n, nblk1 = nblk;
+  std::vector<HeevProblem> p1;
+  if (!p2s.empty()) {
+    int nb2 = 0;
+    heev2s_assign_blocks(p2s.data(), (int)p2s.size(), nb2);
+    const HeevProblem* d2 = static_cast<const HeevProblem*>(st.put(p2s.data(), sizeof(HeevProblem) * p2s.size()));
+    launch_heev2s_backtr(d2, (int)p2s.size(), nb2, maxn2s, s);
+    nblk1 = 0;
+    for (int i = 0; i < n; ++i) {
+      if (is2s[i]) continue;
+      p1.push_back(h[i]);
+      p1.back().bstart = nblk1;
+      nblk1 += (h[i].kmax + BT_WARPS * BT_VPW - 1) / (BT_WARPS * BT_VPW);
+    }
+    nbt = (int)p1.size();
+    dbt = p1.empty() ? nullptr : static_cast<const HeevProblem*>(st.put(p1.data(), sizeof(HeevProblem) * p1.size()));
+  }
+  if (nbt > 0) {
     int mxn = 0;
-    for (int i = 0; i < n; ++i) mxn = std::max(mxn, h[i].n);
+    for (int i = 0; i < n; ++i)
+      if (!is2s[i]) mxn = std::max(mxn, h[i].n);
     if (mxn <= 256) {
       func_smem(heev_backtr_blk<4, BT_VPW>, backtr_smem_bytes(256));
       func_smem(heev_backtr_blk<6, BT_VPW>, backtr_smem_bytes(256));
       func_smem(heev_backtr_blk<8, BT_VPW>, backtr_smem_bytes(256));
-      if (mxn <= 128) launch_k(heev_backtr_blk<4, BT_VPW>, nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s, d, n);
-      else if (mxn <= 192) launch_k(heev_backtr_blk<6, BT_VPW>, nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s, d, n);
-      else launch_k(heev_backtr_blk<8, BT_VPW>, nblk, BT_WARPS * 32, backtr_smem_bytes(mxn), s, d, n);
+      if (mxn <= 128) launch_k(heev_backtr_blk<4, BT_VPW>, nblk1, BT_WARPS * 32, backtr_smem_bytes(mxn), s, dbt, nbt);
+      else if (mxn <= 192) launch_k(heev_backtr_blk<6, BT_VPW>, nblk1, BT_WARPS * 32, backtr_smem_bytes(mxn), s, dbt, nbt);
+      else launch_k(heev_backtr_blk<8, BT_VPW>, nblk1, BT_WARPS * 32, backtr_smem_bytes(mxn), s, dbt, nbt);
     } else {
-      launch_k(heev_backtr, (total * 32 + 255) / 256, 256, 0, s, d, n, total);
+      int tot1 = 0;
+      for (int i = 0; i < n; ++i)
+        if (!is2s[i]) tot1 += h[i].kmax;
+      launch_k(heev_backtr, (tot1 * 32 + 255) / 256, 256, 0, s, dbt, nbt, tot1);
     }
   }
   launch_k(heev_unscale, (n + 127) / 128, 128, 0, s, d, n, 2);
