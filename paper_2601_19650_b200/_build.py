@@ -12,6 +12,7 @@ SOURCES = ["gemm.cu", "heev.cu", "heev2s.cu", "chfsi.cu", "chol.cu", "misc.cu", 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("TCBC_NVCC_FLAGS", "").split()   # A/B builds (tools/), empty by default
 
 
 def _stale() -> bool:

@@ -45,6 +45,16 @@ enum { OP_N = 0, OP_T = 1, OP_R = 2 /*conj, no transpose*/, OP_C = 3 /*conj tran
 // leg fastest); element offsets are sum_leg index * stride with per-operand strides
 // (am, ak for A; bk, bn for B; cm, cn for C).  conjA / conjB conjugate the operand.
 constexpr int GEMM_MAXD = 6;
+// Coordinate rule of one operand's TMA tensor map (gemm.cu, tma_fold): dim d of the map is a
+// leg of the operand's row multi-index (m for A, n for B) or of its k multi-index (bit d of
+// kmask); for a box starting at row x / contraction index k its coordinate is
+// (x_or_k / div[d]) % mod[d] (mod 0: none), doubled for dim 0 (counted in doubles).
+struct TmaDims {
+  int rank, kmask;
+  int chunks;   // boxes per stage: 1, or one per 8 rows (row leg ragged), each 1 KB further on
+  int pad_;
+  int div[5], mod[5];
+};
 struct GemmProblem {
   const cplx* A;
   const cplx* B;
@@ -65,6 +75,11 @@ struct GemmProblem {
   cplx* ws;            // filled by the launcher: ksplit x M x N partial products
   int* exp_out;        // may be null: atomicMax of the binary exponents of the written C
                        // entries (the producer side of pow2 range control)
+  // TMA staging (filled by the launcher): tma >= 0 is the index of this problem's operand
+  // tensor maps in the launch's map array (A at 2*tma, B at 2*tma + 1); -1 = cp.async path
+  int tma;
+  int tma_pad_;
+  TmaDims ta, tb;
 };
 // Device scratch for the launchers (stream-ordered bump memory owned by the caller).
 struct Scratch {
