@@ -893,10 +893,25 @@ bool tma_problem(GemmProblem& p, bool akm, bool bnm, int tm, int tn, CUtensorMap
   Leg m[GEMM_MAXD], n[GEMM_MAXD], ka[GEMM_MAXD], kb[GEMM_MAXD];
   const int nm = norm_legs(p.nm, p.md, p.am, m);
   const int nka = norm_legs(p.nk, p.kd, p.ak, ka);
-  if (!tma_operand(p.A, m, nm, ka, nka, akm, tm, p.ta, maps2[0])) return false;
   const int nn = norm_legs(p.nn, p.nd, p.bn, n);
   const int nkb = norm_legs(p.nk, p.kd, p.bk, kb);
-  return tma_operand(p.B, n, nn, kb, nkb, !bnm, tn, p.tb, maps2[1]);
+  const bool okA = tma_operand(p.A, m, nm, ka, nka, akm, tm, p.ta, maps2[0]);
+  const bool okB = okA && tma_operand(p.B, n, nn, kb, nkb, !bnm, tn, p.tb, maps2[1]);
+  static const bool dbg = getenv("TTN_DEBUG_TMA") != nullptr;
+  if (dbg && !okB) {   // the folds that fail, once per shape
+    thread_local std::unordered_map<std::string, int> seen;
+    auto legs = [](const Leg* L, int c) {
+      std::string o;
+      for (int j = 0; j < c; ++j) o += std::to_string(L[j].ext) + ":" + std::to_string(L[j].stride) + " ";
+      return o;
+    };
+    const std::string k = std::string(okA ? "B" : "A") + " tile " + std::to_string(tm) + "x" + std::to_string(tn) +
+                          (okA ? " n[" + legs(n, nn) + "] k[" + legs(kb, nkb) + "] row_unit=" + std::to_string(!bnm)
+                               : " m[" + legs(m, nm) + "] k[" + legs(ka, nka) + "] row_unit=" + std::to_string(akm));
+    if (seen[k]++ == 0)
+      fprintf(stderr, "[tma-fail] %s MNK %dx%dx%d\n", k.c_str(), p.M, p.N, p.K);
+  }
+  return okB;
 }
 
 // CTA tile shapes (BM x BN); warp tiles 32x32 except the 16-wide skinny shapes (32x16, 16x32)
