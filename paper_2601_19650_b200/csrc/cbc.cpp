@@ -1196,8 +1196,10 @@ void apply_core(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s* co
 // generic apply are min(max_bond, m, n), known from the shapes alone; the schedule is planned
 // with those ranks and checked on the device (SpecDev), so an apply needs ONE host
 // synchronisation (its results) instead of one per level.  A speculative apply that succeeded
-// is captured as a CUDA graph (keyed by shapes and input addresses) and later applies on the
-// same inputs replay it: no host planning, one graph launch.  A failed check (rank-deficient
+// is captured as a CUDA graph (keyed by shapes) against graph-owned copies of its inputs;
+// later applies of the same shapes copy their inputs into those buffers (device to device,
+// stream ordered) and replay it: no host planning, one graph launch -- also for inputs created
+// afresh for every apply (the end-to-end path: ttn_create from host buffers).  A failed check (rank-deficient
 // or tolerance-truncated data) discards the result and re-runs the synchronised schedule;
 // those shapes are then never speculated again on this ctx.
 struct GraphEntry {
@@ -1205,6 +1207,8 @@ struct GraphEntry {
   cudaGraphExec_t ex = nullptr;
   char* desc = nullptr;           // device descriptors of every launch (uploaded once)
   cplx* outbuf = nullptr;         // the outputs, copied to fresh handles after each replay
+  cplx* inbuf = nullptr;          // graph-owned inputs (the caller's are copied in per replay)
+  std::vector<ttn_s*> in_ops, in_sts;   // clones of the capture's inputs; data points into inbuf
   char* host = nullptr;           // pinned result block (SpecRes)
   std::vector<ttn_s*> tmpl;       // output shapes; data points into outbuf (not owned)
   std::vector<FlopAcc> flops;
@@ -1232,6 +1236,11 @@ void destroy_entry(ttn_ctx_s* ctx, GraphEntry* e) {
   if (e->g) cudaGraphDestroy(e->g);
   if (e->desc) cudaFree(e->desc);
   if (e->outbuf) ctx->put(e->outbuf);
+  if (e->inbuf) ctx->put(e->inbuf);
+  for (auto* t : e->in_ops) delete t;   // data belongs to inbuf
+  for (auto* t : e->in_sts) delete t;
+  e->in_ops.clear();
+  e->in_sts.clear();
   if (e->host) cudaFreeHost(e->host);
   for (auto* t : e->tmpl) delete t;   // data belongs to outbuf
   e->tmpl.clear();
@@ -1301,13 +1310,30 @@ std::unique_ptr<GraphEntry> capture(ttn_ctx_s* ctx, int nb, const ttn_s* const* 
     destroy_entry(ctx, e.get());
     return nullptr;
   }
+  int64_t in_elems = 0;
+  for (int b = 0; b < nb; ++b) in_elems += ops[b]->total + sts[b]->total;
   try {
     e->outbuf = static_cast<cplx*>(ctx->get(sizeof(cplx) * std::max<int64_t>(out_elems, 1)));
+    e->inbuf = static_cast<cplx*>(ctx->get(sizeof(cplx) * std::max<int64_t>(in_elems, 1)));
   } catch (...) {
     destroy_entry(ctx, e.get());
     return nullptr;
   }
-  TTN_CUDA(cudaStreamSynchronize(ctx->stream));   // outbuf allocation complete before capture
+  {   // the graph reads its own copies of the inputs
+    int64_t off = 0;
+    auto clone = [&](const ttn_s* t) {
+      ttn_s* c = new ttn_s(*t);
+      c->data = e->inbuf + off;
+      off += t->total;
+      TTN_CUDA(cudaMemcpyAsync(c->data, t->data, sizeof(cplx) * t->total, cudaMemcpyDeviceToDevice, ctx->stream));
+      return c;
+    };
+    for (int b = 0; b < nb; ++b) {
+      e->in_ops.push_back(clone(ops[b]));
+      e->in_sts.push_back(clone(sts[b]));
+    }
+  }
+  TTN_CUDA(cudaStreamSynchronize(ctx->stream));   // outbuf / inbuf ready before capture
   CaptureStager cs(e->desc, cap);
   int64_t used = 0;
   CoreCtl cc;
@@ -1329,7 +1355,8 @@ std::unique_ptr<GraphEntry> capture(ttn_ctx_s* ctx, int nb, const ttn_s* const* 
   bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
   if (ok) {
     try {
-      apply_core(ctx, nb, ops, sts, max_bond, 0.0, outs.data(), nullptr, cc);
+      std::vector<const ttn_s*> co(e->in_ops.begin(), e->in_ops.end()), cs_(e->in_sts.begin(), e->in_sts.end());
+      apply_core(ctx, nb, co.data(), cs_.data(), max_bond, 0.0, outs.data(), nullptr, cc);
     } catch (...) {
       ok = false;
     }
@@ -1365,9 +1392,17 @@ std::unique_ptr<GraphEntry> capture(ttn_ctx_s* ctx, int nb, const ttn_s* const* 
 }
 
 // one replay; false when the device check failed (outputs discarded)
-bool replay(ttn_ctx_s* ctx, GraphEntry* e, int nb, const ttn_s* ref, ttn_s** outs, ttn_cbc_report* reps) {
+bool replay(ttn_ctx_s* ctx, GraphEntry* e, int nb, const ttn_s* const* ops, const ttn_s* const* sts, ttn_s** outs,
+            ttn_cbc_report* reps) {
   auto t0 = std::chrono::steady_clock::now();
   ctx->host_syncs = 0;
+  for (int b = 0; b < nb; ++b) {   // this apply's inputs into the graph's buffers
+    TTN_CUDA(cudaMemcpyAsync(e->in_ops[b]->data, ops[b]->data, sizeof(cplx) * ops[b]->total, cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    TTN_CUDA(cudaMemcpyAsync(e->in_sts[b]->data, sts[b]->data, sizeof(cplx) * sts[b]->total, cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  }
+  const ttn_s* ref = sts[0];
   TTN_CUDA(cudaGraphLaunch(e->ex, ctx->stream));
   add_launches(e->launches);
   for (int b = 0; b < nb; ++b) {
@@ -1418,16 +1453,12 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
     apply_core(ctx, nb, ops, sts, max_bond, tol, outs, reps, sync_cc);
     return;
   }
-  std::vector<int64_t> gkey = skey;
-  for (int b = 0; b < nb; ++b) {
-    gkey.push_back(reinterpret_cast<int64_t>(ops[b]->data));
-    gkey.push_back(reinterpret_cast<int64_t>(sts[b]->data));
-  }
+  const std::vector<int64_t>& gkey = skey;
   if (ctx->graphs) {
     auto it = G.map.find(gkey);
     if (it != G.map.end()) {
       it->second->last_use = ++G.tick;
-      if (replay(ctx, it->second.get(), nb, sts[0], outs, reps)) return;
+      if (replay(ctx, it->second.get(), nb, ops, sts, outs, reps)) return;
       destroy_entry(ctx, it->second.get());
       G.map.erase(it);
       G.failed.insert(tkey);
@@ -1464,8 +1495,8 @@ void cbc_apply_impl(ttn_ctx_s* ctx, int nb, const ttn_s* const* ops, const ttn_s
   }
   const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   fill_reports(reps, nb, ctx->spec_host, cc.flops, cc.maxb, cc.peak, secs, ctx->host_syncs);
-  // capture on the second successful speculative apply of the same key (inputs that are
-  // created afresh for every apply, e.g. from host buffers, never pay for a capture)
+  // capture on the second successful speculative apply of the same shapes (a one-off apply
+  // never pays for a capture)
   if (ctx->graphs && !cc.host_synced && !G.nograph.count(gkey) && !G.seen.count(gkey)) {
     if (G.seen.size() >= 256) G.seen.clear();
     G.seen.insert(gkey);

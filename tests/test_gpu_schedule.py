@@ -71,6 +71,29 @@ def test_graph_replay_tracks_new_inputs_and_batches(P):
         ctx.close()
 
 
+def test_graph_keyed_on_shapes_replays_fresh_inputs(P):
+    """The graph is keyed on shapes only: applies on fresh handles with new data (the
+    end-to-end path) replay it after copying their inputs into the graph's buffers; every
+    result equals the synchronised schedule's on the same input, bit for bit."""
+    ctx = P.Context(0)
+    try:
+        insts = [W.make_config(3, seed=s) for s in (20, 21, 22, 20, 23)]
+        got = []
+        for inst in insts:   # speculative, speculative + capture, replay x3 (fresh handles each)
+            op, st = gpu_pair(P, ctx, inst)
+            out, rep = P.cbc_apply(ctx, op, st, inst.max_bond)
+            assert rep["host_syncs"] == 1, rep
+            got.append(_tensors(P, out))
+        P.ttn_ctx_set_schedule(ctx, False, False)
+        for inst, g in zip(insts, got):
+            op, st = gpu_pair(P, ctx, inst)
+            ref, _ = P.cbc_apply(ctx, op, st, inst.max_bond)
+            assert all(np.array_equal(x, y) for x, y in zip(g, _tensors(P, ref)))
+        assert all(np.array_equal(x, y) for x, y in zip(got[0], got[3]))   # same data, same result
+    finally:
+        ctx.close()
+
+
 def test_rank_deficient_falls_back(P):
     """Circuit layers are rank deficient (exact zeros in the Gram spectra): the device check
     fails, the apply re-runs synchronised, and the result equals the oracle's."""
