@@ -196,7 +196,8 @@ struct Job {
 
 bool chfsi_applicable(int n, int kmax) {
   const int p = chfsi_block(n, kmax);
-  return n > kLargeN && p <= 512 && 2 * p <= n;
+  static const int lo = [] { const char* e = getenv("TTN_CHFSI_MIN_N"); return e ? atoi(e) : kLargeN; }();
+  return n > lo && p <= 512 && 2 * p <= n;
 }
 
 int chfsi_block(int n, int kmax) {
