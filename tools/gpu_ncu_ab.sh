@@ -1,5 +1,6 @@
 #!/bin/bash
-# ncu of zgemm launches, TMA on / off: raw CSV only (reports deleted).  C=config SKIP CNT
+# ncu --set full of zgemm launches with TMA staging on / off (TTN_GEMM_TMA): raw and source-page
+# CSV only, the reports are deleted on the box.  C=config SKIP=launches to skip CNT=launches
 mkdir -p gpurun_out/tma
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/tma/build.log 2>&1 || { tail -30 gpurun_out/tma/build.log; exit 1; }
 for t in 1 0; do
