@@ -29,7 +29,7 @@ namespace tcbc {
 namespace {
 
 struct Fac {
-  cplx* p = nullptr;   // [k, a, b] row-major
+  cplx* p = nullptr;   // [k, b, a] row-major (fac_ba(), the default; TTN_FAC_BA=0: [k, a, b])
   int64_t k = 0, a = 0, b = 0;
 };
 
@@ -101,6 +101,11 @@ struct SpecDev {
   bool* host_synced;   // set when a stage had to synchronise anyway (Chebyshev solver)
 };
 
+bool fac_ba() {
+  static const bool v = [] { const char* e = getenv("TTN_FAC_BA"); return e == nullptr || atoi(e) != 0; }();
+  return v;
+}
+
 Task node_task(const ttn_s* st, const ttn_s* op, int i, const std::map<int, const Fac*>& facs, int open_leg,
                cplx* out) {
   Task t;
@@ -118,16 +123,27 @@ Task node_task(const ttn_s* st, const ttn_s* op, int i, const std::map<int, cons
   t.ops.push_back(T);
   t.ops.push_back(O);
   t.out_labels.push_back(L_SIGP);
+  // factors (and the contraction outputs whose Grams make them) order each edge's legs
+  // (operator bond, state bond) -- [k][b][a] -- when fac_ba(): the state bond is then the
+  // unit-stride leg a contraction over it reads, and the kept legs (k, b) merge into one, so
+  // the GEMM operands fold into TMA boxes (the (a, b) order leaves the operator bond
+  // innermost, split from k by the contracted leg)
+  const bool ba = fac_ba();
   for (auto& kv : facs) {
     Operand F;
     F.ptr = kv.second->p;
-    F.dims = {kv.second->k, kv.second->a, kv.second->b};
-    F.labels = {L_F + kv.first, L_A + kv.first, L_B + kv.first};
+    if (ba) {
+      F.dims = {kv.second->k, kv.second->b, kv.second->a};
+      F.labels = {L_F + kv.first, L_B + kv.first, L_A + kv.first};
+    } else {
+      F.dims = {kv.second->k, kv.second->a, kv.second->b};
+      F.labels = {L_F + kv.first, L_A + kv.first, L_B + kv.first};
+    }
     t.ops.push_back(F);
     t.out_labels.push_back(L_F + kv.first);
   }
-  t.out_labels.push_back(L_A + open_leg);
-  t.out_labels.push_back(L_B + open_leg);
+  t.out_labels.push_back((ba ? L_B : L_A) + open_leg);
+  t.out_labels.push_back((ba ? L_A : L_B) + open_leg);
   t.out = out;
   return t;
 }
