@@ -551,13 +551,15 @@ def run_native(args, rank, world, local_rank):
                      "peak_source": FP64_PEAK_SOURCE,
                      "flops": "algorithmic: node contractions at their cheapest pairwise order, Grams as HERK "
                               "(4 n^2 K), factor / S / CholeskyQR / R products (ttn_cbc_report.flops_gemm_min); "
-                              f"zgemm time = CUDA events around every launch set in a profiled pass of {prof_steps} "
-                              "steps right after the timed region (speculative schedule without graphs)",
+                              f"zgemm time = CUDA events around every contraction launch set in a profiled pass of {prof_steps} "
+                              "steps right after the timed region (speculative schedule without graphs); the "
+                              "eigensolver's own GEMMs (Chebyshev filter, Rayleigh-Ritz; n > 512) are timed under heev",
                      "profiled_pass": {"steps": prof_steps, "workers": prof_workers, "ms_per_step": prof_ms / prof_steps,
                                        "applies_per_s": p_applies / (prof_ms / 1000.0)},
                      "algorithmic_flops_per_step": gmin,
                      "kernel_efficiency": {"achieved": ach_exec, "frac": ach_exec / FP64_PEAK_TFLOPS,
-                                           "executed_flops_per_step": gexec,
+                                           "executed_flops_per_step": g["flops"] / prof_steps,
+                                           "planned_contraction_flops_per_step": gexec,
                                            "note": "flops the kernel executes (the planner may pick a costlier "
                                                    "order that runs faster) / zgemm time"},
                      "flops_per_launch": g["flops"] / max(g["launches"], 1),

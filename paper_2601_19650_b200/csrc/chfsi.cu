@@ -258,8 +258,8 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
         g2.beta = make_double2(1.0, 0.0);
         gp2.push_back(g2);
       }
-      gemm_batch(ctx, gp1, st);
-      gemm_batch(ctx, gp2, st);
+      gemm_batch(ctx, gp1, st, "heev");
+      gemm_batch(ctx, gp2, st, "heev");
     }
     for (int pass = 0; pass < 3; ++pass) {
       std::vector<GemmProblem> g1, g2;
@@ -276,10 +276,10 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
         t1.push_back(TrtriProblem{j.Wg, j.Li, w, (int)w, 0});
         g2.push_back(mk_gemm(j.V + c, OP_N, p, j.Li, OP_C, w, j.Q1 + c, p, n, w, w));
       }
-      gemm_batch(ctx, g1, st);
+      gemm_batch(ctx, g1, st, "heev");
       launch_potrf(p1.data(), (int)p1.size(), *ctx->stager, s);
       launch_trtri(t1.data(), (int)t1.size(), *ctx->stager, s);
-      gemm_batch(ctx, g2, st);
+      gemm_batch(ctx, g2, st, "heev");
       for (Job* jp : act) {
         Job& j = *jp;
         const size_t w = (size_t)(j.p - j.c);
@@ -306,10 +306,10 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
       gv.push_back(mk_gemm(j.W, OP_N, p, j.Zt, OP_T, p, j.W2, p, n, p, p));       // W2 = W Z
       rd.push_back(ResDev{j.V2, j.W2, j.theta, j.res, (int)n, (int)p, j.kmax});
     }
-    gemm_batch(ctx, gw, st);
-    gemm_batch(ctx, gh, st);
+    gemm_batch(ctx, gw, st, "heev");
+    gemm_batch(ctx, gh, st, "heev");
     launch_heev(hh.data(), (int)hh.size(), *ctx->stager, s);
-    gemm_batch(ctx, gv, st);
+    gemm_batch(ctx, gv, st, "heev");
     const ResDev* d = static_cast<const ResDev*>(ctx->stager->put(rd.data(), sizeof(ResDev) * rd.size()));
     const long long warps = (long long)rd.size() * maxk;
     launch_k(ritz_residual, (unsigned)((warps * 32 + 255) / 256), 256, 0, s, d, (int)rd.size(), maxk);
@@ -440,7 +440,7 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
         xb[q] = j.V + j.c;
         yb[q] = j.Y + j.c;
       }
-      gemm_batch(ctx, g, st);
+      gemm_batch(ctx, g, st, "heev");
     }
     for (int deg = 2; deg <= mmax; ++deg) {
       std::vector<GemmProblem> g;
@@ -458,7 +458,7 @@ void chfsi_heev(ttn_ctx_s* ctx, std::vector<HeevProblem*>& probs, ExecStats& st)
         sigma[q] = sn;
         std::swap(xb[q], yb[q]);
       }
-      gemm_batch(ctx, g, st);
+      gemm_batch(ctx, g, st, "heev");
     }
     // the newest filtered tail is yb; the locked columns live in V[:, 0:c]: bring it there
     for (size_t q = 0; q < act.size(); ++q) {

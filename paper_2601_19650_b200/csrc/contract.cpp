@@ -333,7 +333,7 @@ double gemm_flops(const GemmProblem& g) {
   return g.sym ? 4.0 * (double)g.M * (g.M + 1) * g.K : 8.0 * (double)g.M * g.N * g.K;
 }
 
-void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st) {
+void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st, const char* family) {
   HostScope hs_("gemm_batch");
   for (auto& g : probs) st.flops += gemm_flops(g);
   static const bool dbg = getenv("TTN_DEBUG_GEMM") != nullptr;
@@ -358,7 +358,7 @@ void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st) 
     fprintf(stderr, "\n");
   }
   ArenaScratch ws(ctx->scratch);
-  if (!probs.empty()) launch_gemm(probs.data(), (int)probs.size(), *ctx->stager, ctx->stream, &ws);
+  if (!probs.empty()) launch_gemm(probs.data(), (int)probs.size(), *ctx->stager, ctx->stream, &ws, family);
 }
 
 GemmProblem mk_gemm(const cplx* A, int opA, long long lda, const cplx* B, int opB, long long ldb, cplx* C,

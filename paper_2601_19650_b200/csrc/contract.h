@@ -37,8 +37,9 @@ struct ExecStats {
 
 void contract_batch(ttn_ctx_s* ctx, std::vector<Task>& tasks, ExecStats& st);
 
-// Convenience: grouped GEMM with host bookkeeping of flops.
-void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st);
+// Convenience: grouped GEMM with host bookkeeping of flops.  `family` is the profiler family the
+// launch is timed under (the eigensolver's own GEMMs go under "heev", not the contraction's "zgemm").
+void gemm_batch(ttn_ctx_s* ctx, std::vector<GemmProblem>& probs, ExecStats& st, const char* family = "zgemm");
 
 // Algorithmic flops of one problem (8 per complex MAC; Hermitian products count the lower half).
 double gemm_flops(const GemmProblem& g);
