@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--workers", type=int, default=None, help="concurrent sub-batches (ttn_ctx_set_workers)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="short run for ncu: no e2e/cpu/clocks")
+    ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi clock sampling interval (0: off)")
     return ap.parse_args()
 
 
@@ -101,9 +102,10 @@ def aggregate(ms, flops, applies, world, partitioned, device):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    def __init__(self, path):
+    def __init__(self, path, interval_ms=100):
         self.path = path
         self.p = None
+        self.interval_ms = interval_ms
 
     def start(self):
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -111,7 +113,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.f = open(self.path, "w")
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -348,7 +350,8 @@ def run_native(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")) if not args.quick else None
+    clocks = (ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv"), args.clock_ms)
+              if not args.quick and args.clock_ms > 0 else None)
     if clocks:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         clocks.start()
@@ -375,6 +378,12 @@ def run_native(args, rank, world, local_rank):
         dist.barrier()
     launches = P.ttn_launch_count() - lc0
     clk = clocks.stop(local_rank) if clocks else None
+    # what the last timed step produced (a cheap sanity record: a corrupted run shows up as
+    # norms away from the untimed pass's or as bonds grown to max_bond)
+    timed_result = {"max_bond": max(r["max_bond"] for r in last["reps"]),
+                    "norm_min": min(r["norm"] for r in last["reps"]),
+                    "norm_max": max(r["norm"] for r in last["reps"]),
+                    "eps2_sum": sum(r["discarded_weight_sum"] for r in last["reps"])}
     # profiled pass: graphs off so the events bracket each launch set; one stream (concurrent
     # worker sub-batches would stretch each kernel's event interval by sharing the GPU)
     prof_steps = args.steps if cfg in (3, 4) else min(args.steps, 5)
@@ -568,6 +577,7 @@ def run_native(args, rank, world, local_rank):
                      "traffic_source": f"profiles/ncu_zgemm_traffic_r02_c{cfg}.json: DRAM read+write of every "
                                        "zgemm_grouped kernel of one step (ncu, cold-cache replays) / launch sets per step"},
         "kernels": kern,
+        "timed_result": timed_result,
         "gpu_launches": int(launches),
         "clocks": clk,
         "e2e": e2e,

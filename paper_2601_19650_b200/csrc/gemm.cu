@@ -211,6 +211,7 @@ __device__ __forceinline__ void tma_producer(const GemmProblem* __restrict__ pro
   constexpr unsigned ABYTES = BM * BK * 16, BBYTES = BN * BK * 16;
   unsigned g = 0;
   int pi = -1;
+  const CUtensorMap* last = nullptr;
   for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     if (pi < 0 || tile < probs[pi].tile_start || tile >= probs[pi].tile_start + probs[pi].tiles_mn * probs[pi].ksplit)
       pi = find_problem(probs, nprob, tile);
@@ -223,9 +224,15 @@ __device__ __forceinline__ void tma_producer(const GemmProblem* __restrict__ pro
     const int rowc = lane < 10 && !kdim ? tma_coord(D, dd, lane < 5 ? T.m0 : T.n0) : 0;
     const int ra = P.ta.rank, rb = P.tb.rank;
     const CUtensorMap* mA = maps + 2 * P.tma;
-    if (lane == 0) {
+    if (lane == 0 && mA != last) {
+      // the maps were copied into the (reused) descriptor ring by an H2D copy -- a write the
+      // tensormap proxy must be ordered after, or the TMA unit may still hold a descriptor an
+      // earlier launch staged at the same address
+      asm volatile("fence.proxy.tensormap::generic.acquire.sys [%0], 128;" ::"l"(mA) : "memory");
+      asm volatile("fence.proxy.tensormap::generic.acquire.sys [%0], 128;" ::"l"(mA + 1) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(mA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(mA + 1) : "memory");
+      last = mA;
     }
     for (int Tk = 0; Tk < T.ktiles; ++Tk, ++g) {
       const unsigned slot = g % ST;
@@ -761,6 +768,20 @@ bool tma_enabled() {
   return on;
 }
 
+// Problems below this many complex MACs, or with K below TTN_TMA_MIN_K, stay on the cp.async
+// kernels (A/B knobs, default 0: every problem whose operands fold).  Measured: any threshold
+// that moves config-3 / config-2 problems off TMA costs 2-7% there; config 5's run-to-run
+// spread (host-bound, 800-2400 applies/s with and without TMA) hides any effect.
+double tma_min_mnk() {
+  static const double v = [] { const char* e = getenv("TTN_TMA_MIN_MNK"); return e ? atof(e) : 0.0; }();
+  return v;
+}
+
+int tma_min_k() {
+  static const int v = [] { const char* e = getenv("TTN_TMA_MIN_K"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
 CUtensorMapL2promotion l2prom() {
   static const int v = [] { const char* e = getenv("TTN_TMA_L2"); return e ? atoi(e) : 2; }();
   return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
@@ -879,10 +900,13 @@ bool tma_operand(const cplx* base, const Leg* rows, int nr, const Leg* ks, int n
     est[j] = 1;
     if (j > 0) gstr[j - 1] = key.stride[j];
   }
-  const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)d, const_cast<cplx*>(base), gdim,
-                                 gstr, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                 l2prom(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return false;
+  auto encode = [&](CUtensorMap& out) {
+    HostScope hs_("tma_encode");
+    return encode_fn()(&out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)d, const_cast<cplx*>(base), gdim, gstr, box,
+                       est, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2prom(),
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!encode(map)) return false;
   if (cache.size() > (1u << 16)) cache.clear();
   cache.emplace(key, map);
   return true;
@@ -1038,7 +1062,7 @@ void launch_gemm(GemmProblem* h, int n, Stager& st, cudaStream_t s, Scratch* ws,
       }
     }
     p.tma = -1;
-    if (use_tma) {
+    if (use_tma && p.K >= tma_min_k() && (double)p.M * p.N * p.K >= tma_min_mnk()) {
       CUtensorMap m2[2];
       if (tma_problem(p, akm, bnm, kShapes[best].bm, kShapes[best].bn, m2)) {
         p.tma = (int)(tmaps.size() / 2);

@@ -1,13 +1,12 @@
 #!/bin/bash
-# config-5 regression hunt (round 2: 2319 -> 1356 applies/s): bench lines under each knob
+# config-5 run-to-run spread: clock sampling interval (nvidia-smi NVML queries during the
+# host-bound timed region) and worker count
 source tools/gpu_ab.sh
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-export STEPS=3
-run c5_base 5 "" X=1
-run c5_notma 5 "" TTN_GEMM_TMA=0
-run c5_nospec 5 "" TTN_NO_SPECULATE=1
-run c5_no2s 5 "" TTN_HEEV_2S=0
-run c5_facab 5 "" TTN_FAC_BA=0
-run c5_w1 5 "--workers 1" X=1
-run c5_w1_notma 5 "--workers 1" TTN_GEMM_TMA=0
-run c5_nofork 5 "" TTN_GEMM_NO_FORK=1
+export STEPS=5
+for r in 1 2 3; do
+  run c5_clk100_$r 5 "" X=1
+  run c5_clk0_$r 5 "--clock-ms 0" X=1
+  run c5_clk1000_$r 5 "--clock-ms 1000" X=1
+done
+for r in 1 2; do run c5_w1_clk0_$r 5 "--clock-ms 0 --workers 1" X=1; run c5_w8_clk0_$r 5 "--clock-ms 0 --workers 8" X=1; done
